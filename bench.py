@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the bulk inverse-CDF sampling hot path on B200 (one JSON line).
+
+Default workload (N=1): BASELINE.json configs[1] -- 2^28 fp32 odd-grid uniforms
+resident in HBM -> branch-free normal quantile (App C) -> 2^28 fp32
+normal samples in HBM.  One step = one launch over the whole batch.  Inputs
+(1 GiB) exceed the 126 MB L2, so no flush is needed between steps.
+Multi-GPU (torchrun): weak scaling, every rank maps its own 2^28 uniforms
+(Philox counter offset rank * 2^26); no collective on the data path; the
+elapsed time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gsamples/s per GPU and at 8 GPUs (fp32/fp64); % of HBM BW or FP pipe peak"
+UNIT = "Gsamples/s"
+SEED = 0x5EEDC0FFEE123457
+N_MAIN = 1 << 28
+WORKLOAD = ("configs[1]: 2^28 fp32 uniforms streamed from HBM -> branch-free normal quantile "
+            "(App C (5,5), QM_BREAKLESS) -> fp32 normal samples in HBM")
+
+
+# ----------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "MEASURED_PEAKS.json (measured copy bandwidth, burst)"}
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
+
+
+def load_traffic():
+    """Per-element DRAM traffic of each kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """Polls NVML (SM clock, clock-event reasons) every ~2 ms during a timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_reasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1),
+                "n_samples": len(self.samples)}
+
+
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------ reference arm
+def oracle_rate(n_sample, threads, seed=SEED):
+    """Time the oracle (same formula, long double) over a bounded sample on host cores."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle as O
+    from synth import inputs as I
+    u = I.uniform_grid(n_sample, seed, np.float32).astype(np.float64)
+    chunks = np.array_split(u, threads)
+    O.lib()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda c: O.normal_breakless(c, O.C55, 32), chunks))
+    dt = time.perf_counter() - t0
+    return n_sample / dt / 1e9, dt
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args.gpus)
+    if rank != 0:
+        return
+    import oracle as O
+    O.build()
+    threads = os.cpu_count() or 1
+    n_step = 1 << 20                     # bounded sample per step
+    for _ in range(args.warmup):
+        oracle_rate(n_step, threads)
+    ts = []
+    for _ in range(args.steps):
+        _, dt = oracle_rate(n_step, threads)
+        ts.append(dt)
+    total = sum(ts)
+    value = n_step * args.steps / total / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "n": N_MAIN, "reference_sample_per_step": n_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{n_step} fp32 odd-grid uniforms per step -> same formula (App C, "
+                                       f"float-rounded coefficients) in long double, {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def time_steps(fn, steps, warmup, dist=None):
+    import torch
+    for _ in range(warmup):
+        fn()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    return e0.elapsed_time(e1)
+
+
+def max_over_ranks(x, dist):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def variants(Q, torch, peaks, steps=10, warmup=3):
+    """Other §8 rows, each timed alone on one GPU (reported beside the headline)."""
+    out = {}
+    hbm = peaks["hbm_gbs"]
+
+    def rec(name, fn, n, bytes_per, extra=None):
+        ms = time_steps(fn, steps, warmup) / steps
+        r = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n,
+             "hbm_gbs": (bytes_per * n / (ms / 1e3) / 1e9) if bytes_per else 0.0}
+        r["hbm_frac"] = r["hbm_gbs"] / hbm
+        if extra:
+            r.update(extra)
+        out[name] = r
+
+    n = 1 << 28
+    u64 = torch.empty(n, dtype=torch.float64, device="cuda")
+    Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64, out=u64)
+    z64 = torch.empty_like(u64)
+    rec("stream_f64_D13_2^28", lambda: Q.qm_normal_quantile(u64, out=z64), n, 16)
+    zf = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
+    rec("philox_fused_f32_2^32", lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=zf), 1 << 32, 4)
+    del zf
+    zd = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
+    rec("philox_fused_f64_2^31", lambda: Q.qm_normal_philox(1 << 31, SEED, 0, dtype=torch.float64, out=zd),
+        1 << 31, 8)
+    del zd
+    # config 4: Student-t recycling of 2^30 fp64 normals (untimed producer: the fused kernel)
+    zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
+    tt = torch.empty_like(zn)
+    for nu, K, zs in [(4.0, 10, 3.93473), (3.0, 16, 3.5667), (5.0, 16, 4.6506), (10.0, 16, 6.9584)]:
+        rec(f"student_f64_nu{int(nu)}_K{K}_2^30",
+            lambda nu=nu, K=K, zs=zs: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=tt), 1 << 30, 16)
+    ws = torch.empty(4 + 4 * 1024, dtype=torch.float64, device="cuda")
+    rec("moments_f64_2^30", lambda: Q.qm_moments(tt, 4, workspace=ws), 1 << 30, 8)
+    del zn, tt
+    # config 5 building block: Laplace -> normal
+    from synth import inputs as I
+    v = torch.from_numpy(I.laplace(n, dtype=np.float32)).cuda()
+    zo = torch.empty_like(v)
+    rec("exp_to_normal_f32_2^28", lambda: Q.qm_recycle_exp_to_normal(v, out=zo), n, 8)
+    del v, zo
+    # config 1: 2^20 fp64, breakless vs branching baselines (tail-stratified input)
+    u1 = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
+    z1 = torch.empty_like(u1)
+    for name, alg in [("breakless_D13", Q.BREAKLESS), ("as241", Q.AS241), ("acklam", Q.ACKLAM),
+                      ("acklam_refined", Q.ACKLAM_REFINED), ("breakless77", Q.BREAKLESS77)]:
+        rec(f"config1_f64_2^20_{name}", lambda alg=alg: Q.qm_normal_quantile(u1, out=z1, alg=alg), 1 << 20, 16)
+    del u64, z64
+    return out
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args.gpus)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_0901_0638_b200 as Q
+    from paper_0901_0638_b200 import _lib
+    _lib.load()
+    peaks = load_peaks()
+    n = N_MAIN
+
+    # untimed producer: this rank's uniforms (Philox stream, counter offset rank * n/4)
+    u = torch.empty(n, dtype=torch.float32, device="cuda")
+    Q.qm_philox_uniform(n, SEED, rank * (n // 4), out=u)
+    z = torch.empty_like(u)
+    step = lambda: Q.qm_normal_quantile(u, out=z)
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms = time_steps(step, args.steps, args.warmup, dist)
+    ms = max_over_ranks(ms, dist)
+    ms_step = ms / args.steps
+    value = world * n * args.steps / (ms / 1e3) / 1e9
+
+    # roofline of the (only) kernel of the step: 8 algorithmic bytes per sample
+    achieved = 8.0 * n / (ms_step / 1e3) / 1e9
+    traffic = load_traffic().get("k_normal_f32", {}).get("dram_bytes_per_elem")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": (traffic * n if traffic else None),
+            "kernel": "qm::k_normal_f32<ALG_BREAKLESS>", "algorithmic_bytes_per_launch": 8 * n,
+            "peak_source": peaks["source"]}
+
+    # e2e through the public C-ABI host entry point: pinned host in, pinned host out
+    uh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    uh.copy_(u.cpu())
+    zh = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 10))
+    Q.qm_normal_quantile_host(uh, out=zh)
+    if dist is not None:
+        dist.barrier()
+    with ClockSampler(local) as s2:
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            Q.qm_normal_quantile_host(uh, out=zh)
+        t1 = time.perf_counter()
+    e2e_s = max_over_ranks(t1 - t0, dist)
+    e2e = {"value": world * n * e2e_steps / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+           "d2h_bytes_per_step": 4 * n, "steps": e2e_steps, "api": "qm_normal_quantile_host",
+           "gpu_launches": e2e_steps * ((n + (1 << 24) - 1) >> 24), "clocks": s2.summary()}
+    assert torch.equal(zh, z.cpu())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        nsamp = 1 << 25
+        rate, dt = oracle_rate(nsamp, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"2^25 fp32 odd-grid uniforms -> the same formula (App C) in long double "
+                         f"({dt:.1f} s wall on {threads} threads)"}
+
+    var = None
+    if rank == 0 and not args.no_variants:
+        var = variants(Q, torch, peaks)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "n_per_gpu": n, "global_samples_per_step": world * n,
+                           "alg": "QM_BREAKLESS (App C)", "l2": "inputs 1 GiB per GPU > 126 MB L2: no flush",
+                           "parallelism": f"dp{world} (counter-offset shards, no data-path collective)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+                "clocks": sampler.summary(), "variants": var}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,138 @@
+/*
+ * qm.h -- C ABI of the B200-native bulk inverse-CDF sampling library (libqm.so).
+ *
+ * Paper: W. T. Shaw & N. Brickman, "Quantile Mechanics II: Changes of Variables
+ * in Monte Carlo methods and a GPU-Optimized Normal Quantile" (arXiv 0901.0638).
+ * Citations "P:n" are PAPER.md line numbers.
+ *
+ * The problem (§1): given base samples Z with CDF G, produce target
+ * samples A(Z) = F^-1(G(Z)) -- for a uniform base the quantile w(U), F(w(u)) = u.
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Device pointers are caller-owned (allocated by the caller, e.g. torch
+ *    tensors passed by data_ptr()); the library never allocates or frees them
+ *    and never allocates on the hot path (the _host entry point owns private
+ *    staging buffers, see there).
+ *  - Layout: contiguous 1-D arrays, unit stride, of float (QM_F32) or double
+ *    (QM_F64).  16-byte alignment is NOT required; misaligned or ragged arrays
+ *    are handled inside the kernels (128-bit vector body, scalar remainder).
+ *  - n is an int64 element count; n == 0 is a no-op returning QM_OK.
+ *  - stream is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Calls enqueue asynchronously and return without synchronising, except
+ *    qm_*_host which returns after the results are in host memory.
+ *  - In-place (output == input) is allowed; partial overlap is undefined.
+ *  - Errors are reported synchronously, before any launch: QM_EINVAL for a bad
+ *    argument (n < 0, NULL with n > 0, bad enum, nu <= 0, K out of range),
+ *    QM_EUNSUPPORTED for a valid but unsupported combination, QM_ECUDA when the
+ *    launch fails (cudaGetLastError).  There is no per-element status: element
+ *    semantics are IEEE-style (see each function).
+ *  - Determinism: results are bitwise reproducible for the same arguments,
+ *    independent of launch configuration and device count.
+ */
+#ifndef QM_H
+#define QM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QM_ABI_VERSION 1
+
+typedef enum { QM_OK = 0, QM_EINVAL = 1, QM_EUNSUPPORTED = 2, QM_ECUDA = 3 } qm_status;
+typedef enum { QM_F32 = 1, QM_F64 = 2 } qm_precision;
+
+/* Normal-quantile algorithms.
+ *  QM_BREAKLESS    the paper's branch-free rational in the exponential
+ *                  coordinate: App C (5,5) in fp32 ("the algorithm we
+ *                  propose for optimal GPU normal simulation"), App D
+ *                  (13,13) in fp64.
+ *  QM_BREAKLESS77  the (7,7) rational of App A/B.
+ *  QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED  the branching comparison quantiles of
+ *                  the paper's Table 3; fp64 only. */
+typedef enum {
+    QM_BREAKLESS = 0, QM_BREAKLESS77 = 1, QM_AS241 = 2, QM_ACKLAM = 3, QM_ACKLAM_REFINED = 4
+} qm_algorithm;
+
+int         qm_abi_version(void);
+const char *qm_status_string(qm_status s);
+/* number of SMs of the current device (cached per device); -1 on error */
+int         qm_device_sm_count(void);
+
+/* Normal quantile z[i] = w(u[i]), Phi(w(u)) = u.
+ * Breakless algorithms: vv = min(u, 1-u), v = -log(2 vv), z = sign(u - 1/2) v P(v)/Q(v)
+ * (App D).  u in (0,1) -> finite; u = 0 -> -inf; u = 1 -> +inf;
+ * u = 1/2 -> +0; u < 0, u > 1 or NaN -> NaN.  Accuracy: within 4 ulp (fp32) / 2 ulp
+ * (fp64) of the same formula evaluated exactly; the formula itself is within
+ * 4e-7 (App C), 1.1e-15 (App D), 1.06e-9 ((7,7)) of Phi^-1 for v <= 37 (74 for
+ * App D), degrading slowly beyond. */
+qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p,
+                             qm_algorithm alg, void *stream);
+
+/* Antithetic pairs ("always work antithetically"): for each
+ * u[i] in (0,1]: v = -log u[i] ("better, v = -log[u]"), Z = Q(v) >= 0,
+ * z_pairs[2i] = Z, z_pairs[2i+1] = -Z.  2n outputs.  u = 0 -> {+inf, -inf};
+ * u outside [0,1] or NaN -> NaN.  Breakless algorithms only. */
+qm_status qm_normal_antithetic(const void *u, void *z_pairs, int64_t n, qm_precision p,
+                               qm_algorithm alg, void *stream);
+
+/* Counter-based Philox4x32-10 uniforms (row a1; not in the paper, whose rnd()
+ * is a placeholder).  key = (lo32(seed), hi32(seed)); block counter c ->
+ * ctr = (lo32(c), hi32(c), 0, 0).  fp32: u[i] = (2 (w >> 9) + 1) 2^-24 from word
+ * i%4 of block counter_offset + i/4.  fp64: u[i] = (2x + 1) 2^-53 with
+ * x = ((w_{2j} << 32) | w_{2j+1}) >> 12, j = i%2, block counter_offset + i/2.
+ * Values lie on an odd grid: never 0 or 1, 1-u on the grid. */
+qm_status qm_philox_uniform(void *u, int64_t n, qm_precision p, uint64_t seed,
+                            uint64_t counter_offset, void *stream);
+
+/* Fused: z[i] = normal quantile of the i-th Philox uniform above, generated in
+ * registers (no HBM read).  Bitwise equal to qm_philox_uniform followed by
+ * qm_normal_quantile with the same arguments. */
+qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
+                           uint64_t seed, uint64_t counter_offset, void *stream);
+
+/* Recycle standard normal samples into Student-t samples, t = F_nu^-1(Phi(z))
+ * (§3): central series t = z sum_{k=0}^{K} c_k z^{2k} for |z| < zstar
+ * and the two-term tail
+ * t = sqrt(nu) w^(-1/nu)(1 - (nu+1)/(2(nu+2)) w^(2/nu)),
+ * w = (1 - Phi(|z|)) nu sqrt(pi) Gamma(nu/2)/Gamma((nu+1)/2) for |z| >= zstar
+ * (P:267-272), odd in z.  zstar <= 0 selects the paper's 3.93473 when nu = 4 and
+ * K = 10 and is QM_EINVAL otherwise.  1 <= K <= 24; 1 <= nu <= 20
+ * (the coefficient recurrence is ill-conditioned beyond, QM_EUNSUPPORTED).
+ * +-inf -> +-inf, NaN -> NaN. */
+qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p,
+                                 double nu, int K, double zstar, void *stream);
+
+/* Recycle two-sided (Laplace) exponential samples into normal samples
+ * (P:397-405): z = sign(v) Q(|v|) with the breakless rational
+ * and no logarithm.  +-0 -> +-0, +-inf -> +-inf, NaN -> NaN. */
+qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precision p,
+                                   qm_algorithm alg, void *stream);
+
+/* Moment sums S_k = sum_i x_i^k, k = 1..kmax (kmax <= 4), accumulated in fp64
+ * in a fixed order independent of the launch and the device (row a8).
+ * sums_dev is a caller-owned device array of QM_MOMENTS_WORKSPACE doubles:
+ * S_k is written to sums_dev[k-1], the rest is scratch.  Two calls must not
+ * share a workspace concurrently. */
+#define QM_MOMENTS_WORKSPACE (4 + 4 * 1024)
+qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax,
+                     double *sums_dev, void *stream);
+
+/* End-to-end variant of qm_normal_quantile on HOST buffers: copies u in,
+ * computes, copies z out, overlapping the three in chunks on library-owned
+ * streams and pinned/device staging buffers (allocated once per thread and
+ * reused).  Returns after z_host is complete.  Host buffers may be pageable or
+ * pinned. */
+qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n,
+                                  qm_precision p, qm_algorithm alg);
+
+/* Diagnostics: the central-series coefficients c_0..c_K exactly as the
+ * Student kernel receives them (host __float128 recurrence).
+ * c_out has K+1 doubles.  Returns 0 on success. */
+int qm_student_coefficients(double nu, int K, double *c_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QM_H */

@@ -61,6 +61,8 @@ def lib():
             "orc_philox_raw": (None, [P, i64, u64, u64]),
             "orc_philox_uniform_f32": (None, [P, i64, u64, u64]),
             "orc_philox_uniform_f64": (None, [P, i64, u64, u64]),
+            "orc_philox_uniform_f32_at": (None, [P, P, i64, u64, u64]),
+            "orc_philox_uniform_f64_at": (None, [P, P, i64, u64, u64]),
             "orc_ndtri_exact": (None, [P, P, i64]),
             "orc_Qexact": (None, [P, P, i64]),
             "orc_rational": (i32, [P, P, i64, i32, i32]),
@@ -124,6 +126,15 @@ def philox_uniform(n: int, seed: int, counter_offset: int = 0, dtype=np.float32)
         lib().orc_philox_uniform_f32(_p(o), n, seed, counter_offset)
     else:
         lib().orc_philox_uniform_f64(_p(o), n, seed, counter_offset)
+    return o
+
+
+def philox_uniform_at(idx, seed: int, counter_offset: int = 0, dtype=np.float32) -> np.ndarray:
+    """The uniforms at sample indices idx of the stream (for sampled full-size checks)."""
+    idx = _in(idx, np.int64)
+    o = np.zeros(idx.size, dtype)
+    f = lib().orc_philox_uniform_f32_at if dtype == np.float32 else lib().orc_philox_uniform_f64_at
+    f(_p(idx), _p(o), idx.size, seed, counter_offset)
     return o
 
 

@@ -85,3 +85,25 @@ void orc_philox_uniform_f64(double *u, int64_t n, uint64_t seed, uint64_t c0)
         u[i] = (double)ldexpl(num, -53);                  /* exact in double */
     }
 }
+
+/* uniforms at arbitrary sample indices idx[j] of the stream (same layout) */
+void orc_philox_uniform_f32_at(const int64_t *idx, float *u, int64_t n, uint64_t seed, uint64_t c0)
+{
+    uint32_t w[4];
+    for (int64_t j = 0; j < n; ++j) {
+        block_words(seed, c0 + (uint64_t)(idx[j] / 4), w);
+        uint32_t k = w[idx[j] % 4] >> 9;
+        u[j] = (float)ldexp(2.0 * (double)k + 1.0, -24);
+    }
+}
+
+void orc_philox_uniform_f64_at(const int64_t *idx, double *u, int64_t n, uint64_t seed, uint64_t c0)
+{
+    uint32_t w[4];
+    for (int64_t j = 0; j < n; ++j) {
+        block_words(seed, c0 + (uint64_t)(idx[j] / 2), w);
+        int h = (int)(idx[j] % 2);
+        uint64_t x = (((uint64_t)w[2 * h] << 32) | (uint64_t)w[2 * h + 1]) >> 12;
+        u[j] = (double)ldexpl(2.0L * (ld)x + 1.0L, -53);
+    }
+}

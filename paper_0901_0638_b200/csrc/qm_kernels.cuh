@@ -1,0 +1,347 @@
+// qm_kernels.cuh -- __global__ kernels of the hot path (sm_100a).
+//
+// All streaming kernels share one shape:
+//  * grid = k x (SM count) blocks of 256 threads, a warp-uniform grid-stride
+//    loop over warp CHUNKS (32 lanes x V 128-bit vectors), so every branch in
+//    the loop body is warp-uniform -- the paper's divergence argument
+//    turned into a structural property;
+//  * 128-bit streaming loads (ld.global.nc.L1::no_allocate) and stores
+//    (st.global.cs), all loads of a chunk issued before any math;
+//  * one FSETP-AND per element builds a "normal input" predicate; a single
+//    __all_sync vote picks the fast path (no special-value code) or the careful
+//    path for the whole warp.  Grid inputs never leave the fast path;
+//  * the scalar remainder (n % 4, or a misaligned array) runs the careful
+//    scalar code in the same launch.
+#pragma once
+#include "qm_math.cuh"
+
+namespace qm {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------ fp32 normal
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int vec)
+{
+    constexpr int V = 2;                                  // float4 per lane per chunk
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nv = vec ? (n >> 2) : 0;
+    const int64_t nchunks = (nv + 32 * V - 1) / (32 * V);
+    const float4 *u4 = reinterpret_cast<const float4 *>(u);
+    float4 *z4 = reinterpret_cast<float4 *>(z);
+
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {   // warp-uniform trip count
+        float x[4 * V];
+        const int64_t base = c * (32 * V) + lane;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = base + 32 * j;
+            const float4 a = (i < nv) ? ld_stream_f4(u4 + i) : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
+            x[4 * j] = a.x; x[4 * j + 1] = a.y; x[4 * j + 2] = a.z; x[4 * j + 3] = a.w;
+        }
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 4 * V; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= 1.17549435e-38f);
+        float y[4 * V];
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int k = 0; k < 4 * V; k += 2) {
+                const float oa = __fsub_rn(1.0f, x[k]), ob = __fsub_rn(1.0f, x[k + 1]);
+                const float2 lz = neg_log2x_f32x2(fminf(x[k], oa), fminf(x[k + 1], ob));
+                y[k] = apply_sign_f32(rat32<ALG>(lz.x), x[k], oa);
+                y[k + 1] = apply_sign_f32(rat32<ALG>(lz.y), x[k + 1], ob);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4 * V; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = base + 32 * j;
+            if (i < nv) st_stream_f4(z4 + i, make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]));
+        }
+    }
+    // scalar remainder
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = 4 * nv + t;
+    if (i < n) z[i] = nq_f32_careful<ALG>(u[i]);
+    for (int64_t j = i + (int64_t)gridDim.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        z[j] = nq_f32_careful<ALG>(u[j]);
+}
+
+// ------------------------------------------------------------ fp64 normal
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, int vec)
+{
+    constexpr int V = 2;                                  // double2 per lane per chunk
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nv = vec ? (n >> 1) : 0;
+    const int64_t nchunks = (nv + 32 * V - 1) / (32 * V);
+    const double2 *u2 = reinterpret_cast<const double2 *>(u);
+    double2 *z2 = reinterpret_cast<double2 *>(z);
+
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {
+        double x[2 * V];
+        const int64_t base = c * (32 * V) + lane;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = base + 32 * j;
+            const double2 a = (i < nv) ? ld_stream_d2(u2 + i) : make_double2(0.5, 0.5);
+            x[2 * j] = a.x; x[2 * j + 1] = a.y;
+        }
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 2 * V; ++k) ok &= (fmin(x[k], __dadd_rn(1.0, -x[k])) >= 2.2250738585072014e-308);
+        double y[2 * V];
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int k = 0; k < 2 * V; ++k) y[k] = nq_f64_fast<ALG>(x[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 2 * V; ++k) y[k] = nq_f64_careful<ALG>(x[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = base + 32 * j;
+            if (i < nv) st_stream_d2(z2 + i, make_double2(y[2 * j], y[2 * j + 1]));
+        }
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t j = 2 * nv + t; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        z[j] = nq_f64_careful<ALG>(u[j]);
+}
+
+// --------------------------------------------------- Philox uniforms / fused
+// MODE 0: write the uniforms; MODE 1: write the normal quantile of them (fused).
+template <int MODE, int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
+{
+    constexpr int V = 2;                                  // Philox blocks per lane per chunk
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nb = (n + 3) >> 2;                      // Philox blocks
+    const int64_t nchunks = (nb + 32 * V - 1) / (32 * V);
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {
+        const int64_t base = c * (32 * V) + lane;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t b = base + 32 * j;
+            const uint4 w = philox_block(c0 + (unsigned long long)b, seed);
+            float r[4];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            if (MODE == 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) r[k] = u01_f32(ws[k]);
+            } else {
+                float uu[4], om[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) { uu[k] = u01_f32(ws[k]); om[k] = __fsub_rn(1.0f, uu[k]); }
+                const float2 l01 = neg_log2x_f32x2(fminf(uu[0], om[0]), fminf(uu[1], om[1]));
+                const float2 l23 = neg_log2x_f32x2(fminf(uu[2], om[2]), fminf(uu[3], om[3]));
+                r[0] = apply_sign_f32(rat32<ALG>(l01.x), uu[0], om[0]);
+                r[1] = apply_sign_f32(rat32<ALG>(l01.y), uu[1], om[1]);
+                r[2] = apply_sign_f32(rat32<ALG>(l23.x), uu[2], om[2]);
+                r[3] = apply_sign_f32(rat32<ALG>(l23.y), uu[3], om[3]);
+            }
+            const int64_t i = 4 * b;
+            if (vec && i + 3 < n) {
+                st_stream_f4(reinterpret_cast<float4 *>(z + i), make_float4(r[0], r[1], r[2], r[3]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) if (i + k < n) z[i + k] = r[k];
+            }
+        }
+    }
+}
+
+template <int MODE, int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_philox_f64(double *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nb = (n + 1) >> 1;
+    const int64_t nchunks = (nb + 31) / 32;
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {
+        const int64_t b = c * 32 + lane;
+        const uint4 w = philox_block(c0 + (unsigned long long)b, seed);
+        double r0 = u01_f64(w.x, w.y), r1 = u01_f64(w.z, w.w);
+        if (MODE == 1) { r0 = nq_f64_fast<ALG>(r0); r1 = nq_f64_fast<ALG>(r1); }
+        const int64_t i = 2 * b;
+        if (vec && i + 1 < n) {
+            st_stream_d2(reinterpret_cast<double2 *>(z + i), make_double2(r0, r1));
+        } else {
+            if (i < n) z[i] = r0;
+            if (i + 1 < n) z[i + 1] = r1;
+        }
+    }
+}
+
+// -------------------------------------------------- antithetic
+// v = -log u, Z = Q(v); out[2i] = Z, out[2i+1] = -Z.
+template <int ALG>
+QM_DEV float anti_f32_careful(float u)
+{
+    const bool sub = u < 1.17549435e-38f;
+    const float us = sub ? __fmul_rn(u, 16777216.0f) : u;
+    float mag = rat32<ALG>(neg_log2x_f32(us, sub ? -25 : -1));
+    mag = (u == 0.0f) ? __int_as_float(0x7f800000) : mag;
+    mag = __uint_as_float(__float_as_uint(mag) & 0x7fffffffu);            // +0 at u = 1
+    return (u >= 0.0f && u <= 1.0f) ? mag : __int_as_float(0x7fffffff);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_antithetic_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int vec)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nv = vec ? (n >> 2) : 0;
+    const int64_t nchunks = (nv + 31) / 32;
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {
+        const int64_t i = c * 32 + lane;
+        const float4 a = (i < nv) ? ld_stream_f4(reinterpret_cast<const float4 *>(u) + i)
+                                  : make_float4(0.5f, 0.5f, 0.5f, 0.5f);
+        const float x[4] = {a.x, a.y, a.z, a.w};
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ok &= (x[k] >= 1.17549435e-38f) & (x[k] <= 1.0f);
+        float y[4];
+        if (__all_sync(0xffffffffu, ok)) {
+            // -log u: eadj = -1 cancels the factor 2 of neg_log2x
+            const float2 l01 = neg_log2x_f32x2(x[0], x[1], -1);
+            const float2 l23 = neg_log2x_f32x2(x[2], x[3], -1);
+            y[0] = fabsf(rat32<ALG>(l01.x)); y[1] = fabsf(rat32<ALG>(l01.y));
+            y[2] = fabsf(rat32<ALG>(l23.x)); y[3] = fabsf(rat32<ALG>(l23.y));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) y[k] = anti_f32_careful<ALG>(x[k]);
+        }
+        if (i < nv) {
+            float4 *o = reinterpret_cast<float4 *>(z) + 2 * i;
+            st_stream_f4(o, make_float4(y[0], -y[0], y[1], -y[1]));
+            st_stream_f4(o + 1, make_float4(y[2], -y[2], y[3], -y[3]));
+        }
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t j = 4 * nv + t; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const float y = anti_f32_careful<ALG>(u[j]);
+        z[2 * j] = y; z[2 * j + 1] = -y;
+    }
+}
+
+template <int ALG>
+QM_DEV double anti_f64(double u)
+{
+    const bool sub = u < 2.2250738585072014e-308;
+    const double us = sub ? __dmul_rn(u, 18014398509481984.0) : u;
+    double mag = rat64<ALG>(neg_log2x_dd(us, sub ? -55 : -1));
+    mag = (u == 0.0) ? __longlong_as_double(0x7ff0000000000000LL) : mag;
+    mag = fabs(mag);
+    return (u >= 0.0 && u <= 1.0) ? mag : __longlong_as_double(0x7fffffffffffffffLL);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_antithetic_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const double y = anti_f64<ALG>(u[j]);
+        z[2 * j] = y;
+        z[2 * j + 1] = -y;
+    }
+}
+
+// ------------------------------------------- exponential (Laplace) -> normal
+template <int ALG>
+QM_DEV float exp2n_f32(float v)
+{
+    const float a = fabsf(v);
+    float mag = rat32<ALG>(a);
+    mag = (a == __int_as_float(0x7f800000)) ? a : mag;
+    const float r = __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (__float_as_uint(v) & 0x80000000u));
+    return (v == v) ? r : v;
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_exp2n_f32(const float *__restrict__ v, float *__restrict__ z, int64_t n, int vec)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nv = vec ? (n >> 2) : 0;
+    const int64_t nchunks = (nv + 63) / 64;
+    for (int64_t c = gwarp; c < nchunks; c += nwarps) {
+        const int64_t base = c * 64 + lane;
+        float4 a[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int64_t i = base + 32 * j;
+            a[j] = (i < nv) ? ld_stream_f4(reinterpret_cast<const float4 *>(v) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int64_t i = base + 32 * j;
+            const float4 r = make_float4(exp2n_f32<ALG>(a[j].x), exp2n_f32<ALG>(a[j].y),
+                                         exp2n_f32<ALG>(a[j].z), exp2n_f32<ALG>(a[j].w));
+            if (i < nv) st_stream_f4(reinterpret_cast<float4 *>(z) + i, r);
+        }
+    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t j = 4 * nv + t; j < n; j += (int64_t)gridDim.x * blockDim.x) z[j] = exp2n_f32<ALG>(v[j]);
+}
+
+// fp64: for |v| >= 2^40 the polynomials would overflow in double; evaluate the
+// same rational in reversed form, P(v)/Q(v) = Prev(1/v)/Qrev(1/v).
+template <int N>
+QM_DEV double ratio_rev(double v, const double *P, const double *Q)
+{
+    const double w = 1.0 / v;
+    double p = P[0], q = Q[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) { p = __fma_rn(p, w, P[i]); q = __fma_rn(q, w, Q[i]); }
+    return v * (p / q);
+}
+
+template <int ALG>
+QM_DEV double exp2n_f64(double v)
+{
+    const double a = fabs(v);
+    double mag;
+    if (a < 1099511627776.0) {
+        mag = rat64<ALG>(dd{a, 0.0});
+    } else if (a == __longlong_as_double(0x7ff0000000000000LL)) {
+        mag = a;
+    } else {
+        mag = (ALG == ALG_BREAKLESS77) ? ratio_rev<8>(a, kA77P_d, kA77Q_d) : ratio_rev<14>(a, kD13P, kD13Q);
+    }
+    const double r = copysign(mag, v);
+    return (v == v) ? r : v;
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(kThreads)
+k_exp2n_f64(const double *__restrict__ v, double *__restrict__ z, int64_t n)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        const double x = v[j];
+        // warp-uniform fast check
+        const bool ok = fabs(x) < 1099511627776.0;
+        z[j] = __all_sync(__activemask(), ok) ? copysign(rat64<ALG>(dd{fabs(x), 0.0}), x) : exp2n_f64<ALG>(x);
+    }
+}
+
+}  // namespace qm

@@ -1,0 +1,277 @@
+// qm_lib.cu -- the C ABI of libqm.so (include/qm.h): argument validation,
+// launch configuration and the host-buffer pipeline.  Every element of every
+// output is computed by the kernels in qm_kernels.cuh; the host only validates,
+// configures and enqueues.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/qm.h"
+#include "qm_kernels.cuh"
+#include "qm_baselines.cuh"
+#include "qm_student.cuh"
+#include "qm_moments.cuh"
+
+using namespace qm;
+
+namespace {
+
+int sm_count_for_current_device()
+{
+    static std::mutex mu;
+    static std::vector<int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+    if (cache[dev] == 0) {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+        cache[dev] = sms;
+    }
+    return cache[dev];
+}
+
+// blocks: `per_sm` resident blocks per SM, but never more than the work needs
+int grid_for(int64_t work_items, int items_per_block, int per_sm)
+{
+    const int sms = sm_count_for_current_device();
+    int64_t g = (int64_t)(sms > 0 ? sms : 148) * per_sm;
+    const int64_t need = (work_items + items_per_block - 1) / items_per_block;
+    if (need < g) g = need;
+    return (int)(g < 1 ? 1 : g);
+}
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+qm_status launched()
+{
+    return cudaGetLastError() == cudaSuccess ? QM_OK : QM_ECUDA;
+}
+
+bool bad_ptrs(const void *a, const void *b, int64_t n) { return n > 0 && (a == nullptr || b == nullptr); }
+
+}  // namespace
+
+extern "C" {
+
+int qm_abi_version(void) { return QM_ABI_VERSION; }
+
+const char *qm_status_string(qm_status s)
+{
+    switch (s) {
+    case QM_OK: return "ok";
+    case QM_EINVAL: return "invalid argument";
+    case QM_EUNSUPPORTED: return "unsupported combination";
+    case QM_ECUDA: return "CUDA launch failure";
+    }
+    return "unknown status";
+}
+
+int qm_device_sm_count(void) { return sm_count_for_current_device(); }
+
+qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
+{
+    if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;
+    if (p != QM_F32 && p != QM_F64) return QM_EINVAL;
+    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int vec = aligned16(u) && aligned16(z);
+    if (p == QM_F32) {
+        if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+        const int g = grid_for(n, kThreads * 8, 8);
+        if (alg == QM_BREAKLESS)
+            k_normal_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+        else
+            k_normal_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+        return launched();
+    }
+    const int g = grid_for(n, kThreads * 4, 8);
+    switch (alg) {
+    case QM_BREAKLESS:
+        k_normal_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n, vec); break;
+    case QM_BREAKLESS77:
+        k_normal_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n, vec); break;
+    case QM_AS241:
+        k_branchy_f64<ALG_AS241><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
+    case QM_ACKLAM:
+        k_branchy_f64<ALG_ACKLAM><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
+    case QM_ACKLAM_REFINED:
+        k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
+    }
+    return launched();
+}
+
+qm_status qm_normal_antithetic(const void *u, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
+{
+    if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;
+    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p == QM_F32) {
+        const int vec = aligned16(u) && aligned16(z);
+        const int g = grid_for(n, kThreads * 4, 8);
+        if (alg == QM_BREAKLESS)
+            k_antithetic_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+        else
+            k_antithetic_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+    } else {
+        const int g = grid_for(n, kThreads, 8);
+        if (alg == QM_BREAKLESS)
+            k_antithetic_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n);
+        else
+            k_antithetic_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n);
+    }
+    return launched();
+}
+
+static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_algorithm alg,
+                               uint64_t seed, uint64_t c0, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    const int vec = aligned16(z);
+    if (p == QM_F32) {
+        const int g = grid_for((n + 3) / 4, kThreads * 2, 8);
+        if (mode == 0) k_philox_f32<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        else if (alg == QM_BREAKLESS) k_philox_f32<1, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        else k_philox_f32<1, ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+    } else {
+        const int g = grid_for((n + 1) / 2, kThreads, 8);
+        if (mode == 0) k_philox_f64<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+        else if (alg == QM_BREAKLESS) k_philox_f64<1, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+        else k_philox_f64<1, ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+    }
+    return launched();
+}
+
+qm_status qm_philox_uniform(void *u, int64_t n, qm_precision p, uint64_t seed, uint64_t counter_offset, void *stream)
+{
+    if (n < 0 || (n > 0 && u == nullptr) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    return philox_launch(u, n, p, 0, QM_BREAKLESS, seed, counter_offset, stream);
+}
+
+qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg, uint64_t seed,
+                           uint64_t counter_offset, void *stream)
+{
+    if (n < 0 || (n > 0 && z == nullptr) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    return philox_launch(z, n, p, 1, alg, seed, counter_offset, stream);
+}
+
+qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
+{
+    if (n < 0 || bad_ptrs(v, z, n)) return QM_EINVAL;
+    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p == QM_F32) {
+        const int vec = aligned16(v) && aligned16(z);
+        const int g = grid_for(n, kThreads * 8, 8);
+        if (alg == QM_BREAKLESS)
+            k_exp2n_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)v, (float *)z, n, vec);
+        else
+            k_exp2n_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)v, (float *)z, n, vec);
+    } else {
+        const int g = grid_for(n, kThreads, 8);
+        if (alg == QM_BREAKLESS)
+            k_exp2n_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)v, (double *)z, n);
+        else
+            k_exp2n_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)v, (double *)z, n);
+    }
+    return launched();
+}
+
+qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p, double nu, int K,
+                                 double zstar, void *stream)
+{
+    if (n < 0 || bad_ptrs(z, t, n) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (!(nu > 0.0) || K < 1 || K > QM_STUDENT_KMAX) return QM_EINVAL;
+    if (!(zstar > 0.0)) {
+        if (nu == 4.0 && K == 10) zstar = 3.93473;
+        else return QM_EINVAL;
+    }
+    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
+    StudentParams sp;
+    if (!student_params(nu, K, zstar, &sp)) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = grid_for(n, kThreads * 2, 8);
+    if (p == QM_F64) k_student_f64<<<g, kThreads, 0, s>>>((const double *)z, (double *)t, n, sp);
+    else k_student_f32<<<g, kThreads, 0, s>>>((const float *)z, (float *)t, n, sp);
+    return launched();
+}
+
+qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax, double *sums_dev, void *stream)
+{
+    if (n < 0 || (n > 0 && x == nullptr) || sums_dev == nullptr) return QM_EINVAL;
+    if ((p != QM_F32 && p != QM_F64) || kmax < 1 || kmax > 4) return QM_EINVAL;
+    return moments_launch(x, n, p == QM_F64, kmax, sums_dev, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ e2e
+namespace {
+struct HostPipe {
+    cudaStream_t st[2] = {nullptr, nullptr};
+    void *din[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
+    size_t cap = 0;   // bytes per buffer
+    int dev = -1;
+    ~HostPipe()
+    {
+        for (int i = 0; i < 2; ++i) {
+            if (din[i]) cudaFree(din[i]);
+            if (dout[i]) cudaFree(dout[i]);
+            if (st[i]) cudaStreamDestroy(st[i]);
+        }
+    }
+};
+thread_local HostPipe g_pipe;
+}  // namespace
+
+qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, qm_precision p, qm_algorithm alg)
+{
+    if (n < 0 || bad_ptrs(u_host, z_host, n) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (p == QM_F32 && alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    const size_t es = (p == QM_F32) ? 4 : 8;
+    const int64_t chunk = (int64_t)1 << 24;                 // elements per pipeline stage
+    const size_t need = (size_t)chunk * es;
+    HostPipe &hp = g_pipe;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (hp.dev != dev || hp.cap < need) {
+        hp.~HostPipe();
+        new (&hp) HostPipe();
+        for (int i = 0; i < 2; ++i) {
+            if (cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking) != cudaSuccess) return QM_ECUDA;
+            if (cudaMalloc(&hp.din[i], need) != cudaSuccess || cudaMalloc(&hp.dout[i], need) != cudaSuccess)
+                return QM_ECUDA;
+        }
+        hp.cap = need;
+        hp.dev = dev;
+    }
+    const char *hu = (const char *)u_host;
+    char *hz = (char *)z_host;
+    int k = 0;
+    for (int64_t off = 0; off < n; off += chunk, k ^= 1) {
+        const int64_t m = (n - off < chunk) ? (n - off) : chunk;
+        cudaStream_t s = hp.st[k];
+        if (cudaMemcpyAsync(hp.din[k], hu + off * es, m * es, cudaMemcpyHostToDevice, s) != cudaSuccess) return QM_ECUDA;
+        qm_status r = qm_normal_quantile(hp.din[k], hp.dout[k], m, p, alg, s);
+        if (r != QM_OK) return r;
+        if (cudaMemcpyAsync(hz + off * es, hp.dout[k], m * es, cudaMemcpyDeviceToHost, s) != cudaSuccess) return QM_ECUDA;
+    }
+    for (int i = 0; i < 2; ++i)
+        if (cudaStreamSynchronize(hp.st[i]) != cudaSuccess) return QM_ECUDA;
+    return QM_OK;
+}
+
+}  // extern "C"

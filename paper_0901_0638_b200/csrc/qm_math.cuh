@@ -1,0 +1,352 @@
+// qm_math.cuh -- device numerics of the hot path (sm_100a).
+//
+// Paper: Shaw & Brickman, "Quantile Mechanics II" (arXiv 0901.0638); P:n are
+// PAPER.md line numbers.  The kernels evaluate the paper's formulas; the
+// arithmetic SCHEME below (how each formula is evaluated so that the result is
+// within 4 ulp (fp32) / 2 ulp (fp64) of the exactly evaluated formula) is ours
+// and is described in DESIGN.md "Kernels".
+//
+//  fp32 breakless (App B/C):  vv = min(u, 1-u) (exact), z = -log(2 vv) by a
+//    polynomial log in fp32 (<= 1 ulp), then z P(z)/Q(z) with the
+//    float-rounded coefficients evaluated in FP64 (B200 has a full-rate-ish FP64
+//    pipe: 64 lanes/SM), one final rounding to float.  Exhaustive CPU emulation
+//    over the fp32 grid: <= 1.42 ulp.
+//  fp64 breakless (App D):    z = -log(2 vv) as a double-double from a
+//    range-reduced atanh series, compensated (error-free transform) Horner for
+//    the last K steps of P and Q, a double-double quotient and one final
+//    rounding: <= ~0.7 ulp.
+#pragma once
+#include "qm_prim.cuh"
+
+namespace qm {
+
+// ---------------------------------------------------------------- constants
+// App C (5,5), P:792-803 -- float-rounded as the listing declares (`const float`),
+// held in double for the FP64 evaluation.
+__constant__ double kC55P[6] = {
+    (double)(float)1.2533136835212087879, (double)(float)1.9797154223229267471,
+    (double)(float)0.80002295072483916762, (double)(float)0.087403248265958578062,
+    (double)(float)0.0020751409553756572917, (double)(float)4.744820732427972462e-6};
+__constant__ double kC55Q[6] = {
+    1.0, (double)(float)2.0795584360534589311, (double)(float)1.2499328117341603014,
+    (double)(float)0.23668431621373705623, (double)(float)0.0120098270559197768,
+    (double)(float)0.00010590620919921025259};
+// the same coefficients as floats (for the optional fp32 inner Horner steps)
+__constant__ float kC55Pf[6] = {1.2533136835212087879f, 1.9797154223229267471f, 0.80002295072483916762f,
+                                0.087403248265958578062f, 0.0020751409553756572917f, 4.744820732427972462e-6f};
+__constant__ float kC55Qf[6] = {1.0f, 2.0795584360534589311f, 1.2499328117341603014f,
+                                0.23668431621373705623f, 0.0120098270559197768f, 0.00010590620919921025259f};
+
+// App A/B (7,7), P:477-497 / P:755-770: float-rounded (App B) and double (App A)
+#define QM_A77P 1.2533141359896652729, 3.0333178251950406994, 2.3884158540184385711, \
+    0.73176759583280610539, 0.085838533424158257377, 0.0034424140686962222423,       \
+    0.000036313870818023761224, 4.3304513840364031401e-8
+#define QM_A77Q 1.0, 2.9202373175993672857, 2.9373357991677046357, 1.2356513216582148689, \
+    0.2168237095066675527, 0.014494272424798068406, 0.00030617264753008793976,          \
+    1.3141263119543315917e-6
+__constant__ double kA77P_d[8] = {QM_A77P};
+__constant__ double kA77Q_d[8] = {QM_A77Q};
+__constant__ double kA77P_f[8] = {
+    (double)(float)1.2533141359896652729, (double)(float)3.0333178251950406994,
+    (double)(float)2.3884158540184385711, (double)(float)0.73176759583280610539,
+    (double)(float)0.085838533424158257377, (double)(float)0.0034424140686962222423,
+    (double)(float)0.000036313870818023761224, (double)(float)4.3304513840364031401e-8};
+__constant__ double kA77Q_f[8] = {
+    1.0, (double)(float)2.9202373175993672857, (double)(float)2.9373357991677046357,
+    (double)(float)1.2356513216582148689, (double)(float)0.2168237095066675527,
+    (double)(float)0.014494272424798068406, (double)(float)0.00030617264753008793976,
+    (double)(float)1.3141263119543315917e-6};
+
+// App D (13,13), P:821-848 (`const double`)
+__constant__ double kD13P[14] = {
+    1.2533141373154989811, 5.5870183514814983104, 9.9373788223105148469, 9.11745910783758368,
+    4.6865666928347513004, 1.3841649695441184484, 0.23434950424605615377, 0.022306824510199724768,
+    0.0011538603964070818722, 0.000030796620691411567563, 3.9115723028719510263e-7,
+    2.0589573468131996933e-9, 3.3944224725087481454e-12, 7.3936480912071325978e-16};
+__constant__ double kD13Q[14] = {
+    1.00000000000000000000, 4.9577956835689939051, 9.9793129245112074476, 10.574454910639356539,
+    6.4247521669505779535, 2.3008904864351121026, 0.48545999687461771635, 0.059283082737079006352,
+    0.0040618506206078995821, 0.00014919732843986856251, 2.7477061392049947066e-6,
+    2.2815008011613816939e-8, 7.0445790305953963457e-11, 5.1535907808963289678e-14};
+
+// fp32 log: log1p(f) = f + f^2 R(f), f in [-1/3, 1/3); R: Chebyshev fit
+// (tools/fit_log.py), |error of R| < 3.2e-8 -> < 0.2 ulp of log1p.
+#define QM_LR0 -0.5f
+#define QM_LR1 0.33333271741867065f
+#define QM_LR2 -0.24999944865703583f
+#define QM_LR3 0.20007233321666718f
+#define QM_LR4 -0.16673316061496735f
+#define QM_LR5 0.140558123588562f
+#define QM_LR6 -0.12288721650838852f
+#define QM_LR7 0.13748309016227722f
+#define QM_LR8 -0.12422200292348862f
+#define QM_LN2F_HI 0.693145751953125f        // 16 significant bits: e*hi exact for |e| < 256
+#define QM_LN2F_LO 1.428606765330187e-06f
+
+// fp64 log: log1p(f) = 2 atanh(s) = 2s + s^3 T(s^2), s = f/(2+f) in [-0.2, 1/7];
+// T: Chebyshev fit on w in [0, 1/25], relative error < 4e-17 (term is < 1.3% of 2s)
+__constant__ double kLogT[8] = {0.6666666666666666, 0.400000000000078, 0.2857142856733919,
+                                0.22222223037807243, 0.18181738454723026, 0.15388834677801916,
+                                0.1321036048513262, 0.13604015707124079};
+#define QM_LN2_HI 6.93147180369123816490e-01   // trailing zeros: e*hi exact for |e| < 2^11
+#define QM_LN2_LO 1.90821492927058770002e-10
+
+// ------------------------------------------------------------- fp32 pieces
+// z = -log(2 vv) for vv a normal float in (0, 1/2]; `eadj` adds to the binary
+// exponent (used to pre-scale subnormals by 2^24).  <= ~1 ulp.
+QM_DEV float neg_log2x_f32(float vv, int eadj)
+{
+    const int32_t k = (int32_t)(__float_as_uint(vv) - 0x3f2aaaabu);   // 0x3f2aaaab = 2/3
+    const int32_t e = (k >> 23) + 1 + eadj;                             // +1: the factor 2
+    const float m = __uint_as_float(((uint32_t)k & 0x7fffffu) + 0x3f2aaaabu);   // [2/3, 4/3)
+    const float f = __fsub_rn(m, 1.0f);                                 // exact (Sterbenz)
+    float r = __fmaf_rn(QM_LR8, f, QM_LR7);
+    r = __fmaf_rn(r, f, QM_LR6);
+    r = __fmaf_rn(r, f, QM_LR5);
+    r = __fmaf_rn(r, f, QM_LR4);
+    r = __fmaf_rn(r, f, QM_LR3);
+    r = __fmaf_rn(r, f, QM_LR2);
+    r = __fmaf_rn(r, f, QM_LR1);
+    r = __fmaf_rn(r, f, QM_LR0);
+    const float f2 = __fmul_rn(f, f);
+    const float L = __fmaf_rn(f2, r, f);                                // log1p(f)
+    // (float)e without I2F: 1.5*2^23 + e as bits, minus 1.5*2^23 (|e| < 2^22)
+    const float ef = __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
+    float zf = __fmaf_rn(ef, QM_LN2F_HI, L);
+    zf = __fmaf_rn(ef, QM_LN2F_LO, zf);
+    return -zf;
+}
+
+// Two samples at once with packed f32x2 arithmetic (bitwise identical to two
+// calls of neg_log2x_f32 with the same eadj).
+QM_DEV float2 neg_log2x_f32x2(float vva, float vvb, int eadj = 0)
+{
+    const int32_t ka = (int32_t)(__float_as_uint(vva) - 0x3f2aaaabu);
+    const int32_t kb = (int32_t)(__float_as_uint(vvb) - 0x3f2aaaabu);
+    const float2 m = make_float2(__uint_as_float(((uint32_t)ka & 0x7fffffu) + 0x3f2aaaabu),
+                                 __uint_as_float(((uint32_t)kb & 0x7fffffu) + 0x3f2aaaabu));
+    const float2 f = add2(m, make_float2(-1.0f, -1.0f));
+    float2 r = fma2(make_float2(QM_LR8, QM_LR8), f, make_float2(QM_LR7, QM_LR7));
+    r = fma2(r, f, make_float2(QM_LR6, QM_LR6));
+    r = fma2(r, f, make_float2(QM_LR5, QM_LR5));
+    r = fma2(r, f, make_float2(QM_LR4, QM_LR4));
+    r = fma2(r, f, make_float2(QM_LR3, QM_LR3));
+    r = fma2(r, f, make_float2(QM_LR2, QM_LR2));
+    r = fma2(r, f, make_float2(QM_LR1, QM_LR1));
+    r = fma2(r, f, make_float2(QM_LR0, QM_LR0));
+    const float2 f2 = mul2(f, f);
+    const float2 L = fma2(f2, r, f);
+    const float2 ef = add2(make_float2(__int_as_float(0x4B400000 + (ka >> 23) + 1 + eadj),
+                                       __int_as_float(0x4B400000 + (kb >> 23) + 1 + eadj)),
+                           make_float2(-12582912.0f, -12582912.0f));
+    float2 zf = fma2(ef, make_float2(QM_LN2F_HI, QM_LN2F_HI), L);
+    zf = fma2(ef, make_float2(QM_LN2F_LO, QM_LN2F_LO), zf);
+    return make_float2(-zf.x, -zf.y);
+}
+
+// |z P(z)/Q(z)| for the fp32 formulas: coefficients float-rounded, evaluated in
+// FP64 (N coefficients each), rcp seed + one quotient correction, one rounding.
+template <int N>
+QM_DEV float rational_f32path(float z, const double *P, const double *Q)
+{
+    const double zd = (double)z;
+    double p = P[N - 1], q = Q[N - 1];
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {
+        p = __fma_rn(p, zd, P[i]);
+        q = __fma_rn(q, zd, Q[i]);
+    }
+    const double r = rcp_approx_f64(q);
+    double t = __dmul_rn(p, r);
+    const double e = __fma_rn(-q, t, p);
+    t = __fma_rn(e, r, t);
+    return (float)__dmul_rn(zd, t);
+}
+
+// copysign by the sign of (u - (1-u)): +0 at u = 1/2 (P:773, P:855 sgn = +1)
+QM_DEV float apply_sign_f32(float mag, float u, float omu)
+{
+    const uint32_t s = __float_as_uint(__fsub_rn(u, omu)) & 0x80000000u;
+    return __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | s);
+}
+
+// ------------------------------------------------------------- fp64 pieces
+struct dd { double hi, lo; };
+
+// -log(2 vv) as a double-double for vv a normal double in (0, 1/2]
+QM_DEV dd neg_log2x_dd(double vv, int eadj)
+{
+    const int64_t k = (int64_t)(__double_as_longlong(vv) - 0x3FE5555555555555LL);   // 2/3
+    const int64_t e = (k >> 52) + 1 + eadj;
+    const double m = __longlong_as_double((k & 0x000FFFFFFFFFFFFFLL) + 0x3FE5555555555555LL);
+    const double f = __dadd_rn(m, -1.0);                     // exact, [-1/3, 1/3)
+    // s = f / (2 + f) as sh + sl
+    const double dh = __dadd_rn(2.0, f);
+    const double dl = __dadd_rn(f, -__dadd_rn(dh, -2.0));   // Fast2Sum, |2| >= |f|
+    double r = rcp_approx_f64(dh);
+    r = __fma_rn(r, __fma_rn(-dh, r, 1.0), r);               // ~2^-44
+    const double sh = __dmul_rn(f, r);
+    double rem = __fma_rn(-sh, dh, f);
+    rem = __fma_rn(-sh, dl, rem);
+    const double sl = __dmul_rn(rem, r);
+    // log1p(f) = 2 sh + (2 sl + sh^3 T(sh^2))
+    const double w = __dmul_rn(sh, sh);
+    double T = kLogT[7];
+#pragma unroll
+    for (int i = 6; i >= 0; --i) T = __fma_rn(T, w, kLogT[i]);
+    const double l_hi = 2.0 * sh;
+    const double l_lo = __fma_rn(__dmul_rn(sh, w), T, 2.0 * sl);
+    // + e ln2:  a = E*LN2_HI (exact); Fast2Sum(a, l_hi) valid: |a| >= ln2 > |l_hi| or a = 0
+    const double E = (double)e;
+    const double a = __dmul_rn(E, QM_LN2_HI);
+    const double S = __dadd_rn(a, l_hi);
+    const double err = __dadd_rn(l_hi, -__dadd_rn(S, -a));
+    const double lo = __dadd_rn(err, __fma_rn(E, QM_LN2_LO, l_lo));
+    const double t = __dadd_rn(S, lo);
+    const double tl = __dadd_rn(lo, -__dadd_rn(t, -S));
+    return dd{-t, -tl};
+}
+
+// Compensated Horner (error-free transforms) of sum a_i z^i at z = zh + zl,
+// plain FMA for the first N-1-KC steps, compensated for the last KC steps.
+template <int N, int KC>
+QM_DEV dd horner_comp(const double *a, double zh, double zl)
+{
+    double s = a[N - 1], c = 0.0;
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {
+        if (i >= KC) {
+            s = __fma_rn(s, zh, a[i]);
+        } else {
+            const double p = __dmul_rn(s, zh);
+            const double pi = __fma_rn(s, zh, -p);               // TwoProd
+            const double t = __dadd_rn(p, a[i]);                 // TwoSum
+            const double bb = __dadd_rn(t, -p);
+            const double sg = __dadd_rn(__dadd_rn(p, -__dadd_rn(t, -bb)), __dadd_rn(a[i], -bb));
+            c = __fma_rn(c, zh, __fma_rn(s, zl, __dadd_rn(pi, sg)));
+            s = t;
+        }
+    }
+    return dd{s, c};
+}
+
+// z P(z)/Q(z) for a double-double z >= 0, one final rounding
+template <int N, int KC>
+QM_DEV double rational_dd(dd z, const double *P, const double *Q)
+{
+    const dd p = horner_comp<N, KC>(P, z.hi, z.lo);
+    const dd q = horner_comp<N, KC>(Q, z.hi, z.lo);
+    double r = rcp_approx_f64(q.hi);
+    r = __fma_rn(r, __fma_rn(-q.hi, r, 1.0), r);
+    const double q0 = __dmul_rn(p.hi, r);
+    double e = __fma_rn(-q.hi, q0, p.hi);
+    e = __fma_rn(-q0, q.lo, __dadd_rn(e, p.lo));
+    const double dq = __dmul_rn(e, r);
+    return __fma_rn(z.hi, q0, __fma_rn(z.hi, dq, __dmul_rn(z.lo, q0)));
+}
+
+QM_DEV double apply_sign_f64(double mag, double u, double omu)
+{
+    const unsigned long long s = (unsigned long long)__double_as_longlong(__dadd_rn(u, -omu)) & 0x8000000000000000ULL;
+    return __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(mag) & 0x7fffffffffffffffULL) | s));
+}
+
+// ----------------------------------------------------- breakless quantiles
+// Algorithm ids for templates (mirror qm_algorithm)
+enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1 };
+
+template <int ALG>
+QM_DEV float rat32(float z)
+{
+    if (ALG == ALG_BREAKLESS77) return rational_f32path<8>(z, kA77P_f, kA77Q_f);
+    return rational_f32path<6>(z, kC55P, kC55Q);
+}
+
+template <int ALG>
+QM_DEV double rat64(dd z)
+{
+    if (ALG == ALG_BREAKLESS77) return rational_dd<8, 7>(z, kA77P_d, kA77Q_d);
+    return rational_dd<14, 13>(z, kD13P, kD13Q);
+}
+
+// fast path: requires vv = min(u, 1-u) >= 2^-126 (normal, not NaN)
+template <int ALG>
+QM_DEV float nq_f32_fast(float u)
+{
+    const float omu = __fsub_rn(1.0f, u);
+    const float vv = fminf(u, omu);
+    return apply_sign_f32(rat32<ALG>(neg_log2x_f32(vv, 0)), u, omu);
+}
+
+// every input: subnormal vv pre-scaled by 2^24; 0/1 -> -+inf; else NaN
+template <int ALG>
+QM_DEV float nq_f32_careful(float u)
+{
+    const float omu = __fsub_rn(1.0f, u);
+    const float vv = fminf(u, omu);
+    const bool sub = vv < 1.17549435e-38f;
+    const float vs = sub ? __fmul_rn(vv, 16777216.0f) : vv;
+    float mag = rat32<ALG>(neg_log2x_f32(vs, sub ? -24 : 0));
+    mag = (vv == 0.0f) ? __int_as_float(0x7f800000) : mag;
+    const float r = apply_sign_f32(mag, u, omu);
+    return (vv >= 0.0f) ? r : __int_as_float(0x7fffffff);   // NaN, u < 0, u > 1
+}
+
+template <int ALG>
+QM_DEV double nq_f64_fast(double u)
+{
+    const double omu = __dadd_rn(1.0, -u);
+    const double vv = fmin(u, omu);
+    return apply_sign_f64(rat64<ALG>(neg_log2x_dd(vv, 0)), u, omu);
+}
+
+template <int ALG>
+QM_DEV double nq_f64_careful(double u)
+{
+    const double omu = __dadd_rn(1.0, -u);
+    const double vv = fmin(u, omu);
+    const bool sub = vv < 2.2250738585072014e-308;
+    const double vs = sub ? __dmul_rn(vv, 18014398509481984.0) : vv;   // 2^54
+    double mag = rat64<ALG>(neg_log2x_dd(vs, sub ? -54 : 0));
+    mag = (vv == 0.0) ? __longlong_as_double(0x7ff0000000000000LL) : mag;
+    const double r = apply_sign_f64(mag, u, omu);
+    return (vv >= 0.0) ? r : __longlong_as_double(0x7fffffffffffffffLL);
+}
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11); see qm.h for the stream layout.
+QM_DEV uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
+        const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+QM_DEV uint4 philox_block(unsigned long long counter, unsigned long long seed)
+{
+    return philox4x32_10(make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u),
+                         (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+// (2 (w >> 9) + 1) 2^-24: [1,2) float from the top 23 bits, minus (1 - 2^-24), exact
+QM_DEV float u01_f32(uint32_t w)
+{
+    return __fsub_rn(__uint_as_float(0x3f800000u | (w >> 9)), 0x1.fffffep-1f);
+}
+
+// (2x + 1) 2^-53, x = ((hi << 32) | lo) >> 12
+QM_DEV double u01_f64(uint32_t hi, uint32_t lo)
+{
+    const unsigned long long x = (((unsigned long long)hi << 32) | lo) >> 12;
+    return __dadd_rn(__longlong_as_double((long long)(0x3FF0000000000000ULL | x)), -0x1.fffffffffffffp-1);
+}
+
+}  // namespace qm

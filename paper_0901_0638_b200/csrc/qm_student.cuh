@@ -1,0 +1,100 @@
+// qm_student.cuh -- normal -> Student-t recycling kernel.
+//
+//   central  t = z sum_{k=0}^{K} c_k y^k, y = z^2
+//   tail     w = (1 - Phi(|z|)) C_nu, C_nu = nu sqrt(pi) Gamma(nu/2)/Gamma((nu+1)/2),
+//            t = sqrt(nu) w^(-1/nu) (1 - (nu+1)/(2(nu+2)) w^(2/nu))
+//   composite central for |z| < z*, tail for |z| >= z*, odd in z.
+//
+// c_0..c_K come from the recurrence of P:178-188, run on the host in __float128
+// (qm_student_host.cpp): the recurrence cancels terms of size c_i down to
+// c_{i+1}, so double would lose up to 8 digits at nu = 10, K = 16.
+//
+// Device: the central series is a compensated Horner in y carried as a
+// double-double (y = z*z exactly); the tail is evaluated in double-double
+// (log, exp) behind a warp-uniform vote, so it costs nothing when no lane of
+// the warp is in the tail (P(|z| > 3.9) ~ 1e-4 per sample).
+#pragma once
+#include "qm_dd.cuh"
+
+#include "qm_student_params.h"
+
+namespace qm {
+
+QM_DEV double student_central(const StudentParams &sp, double a)
+{
+    const double yh = __dmul_rn(a, a);
+    const double yl = __fma_rn(a, a, -yh);
+    double s = sp.c[sp.K], c = 0.0;
+    for (int i = sp.K - 1; i >= 0; --i) {
+        const double p = __dmul_rn(s, yh);
+        const double pi = __fma_rn(s, yh, -p);
+        const double t = __dadd_rn(p, sp.c[i]);
+        const double bb = __dadd_rn(t, -p);
+        const double sg = __dadd_rn(__dadd_rn(p, -__dadd_rn(t, -bb)), __dadd_rn(sp.c[i], -bb));
+        c = __fma_rn(c, yh, __fma_rn(s, yl, __dadd_rn(pi, sg)));
+        s = t;
+    }
+    return __fma_rn(a, s, __dmul_rn(a, c));
+}
+
+QM_DEV double student_tail(const StudentParams &sp, double a)
+{
+    // log w = log(erfc(a/sqrt2)) + log(C_nu/2); erfc(x) = exp(-x^2) erfcx(x)
+    const double x = a * 0.70710678118654752440;
+    const double xh = __dmul_rn(a, 0.70710678118654752440);
+    const double xl = __fma_rn(a, 0.70710678118654752440, -xh) + a * (-4.8336466567264567e-17);
+    (void)x;
+    const dd x2 = dd_mul(dd{xh, xl}, dd{xh, xl});
+    const dd lx = dd_log(erfcx(xh));
+    dd logw = dd_add(dd{-x2.hi, -x2.lo}, lx);
+    logw = dd_add(logw, dd{sp.logC_hi, sp.logC_lo});
+    // w^(-1/nu), w^(2/nu)
+    const dd e1 = dd_exp(dd_mul_d(logw, -sp.inv_nu));
+    const dd e2 = dd_exp(dd_mul_d(logw, sp.two_over_nu));
+    const dd corr = dd_add_d(dd_mul_d(e2, -sp.acoef), 1.0);
+    const dd t = dd_mul(dd_mul_d(e1, sp.sqrt_nu), corr);
+    return t.hi + t.lo;
+}
+
+QM_DEV double student_map(const StudentParams &sp, double z, bool any_tail)
+{
+    const double a = fabs(z);
+    double t = student_central(sp, a);
+    if (any_tail) {
+        const double tt = student_tail(sp, fmax(a, 1.0));
+        t = (a >= sp.zstar) ? tt : t;
+    }
+    t = (a == __longlong_as_double(0x7ff0000000000000LL)) ? a : t;
+    const double r = copysign(t, z);
+    return (z == z) ? r : z;
+}
+
+__global__ void __launch_bounds__(256)
+k_student_f64(const double *__restrict__ z, double *__restrict__ t, int64_t n, const __grid_constant__ StudentParams sp)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) / 32 * 32;                     // warp-uniform trip count
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        const double x = (i < n) ? z[i] : 0.0;
+        const bool tail = !(fabs(x) < sp.zstar);                    // NaN votes for the careful path too
+        const bool any = __any_sync(0xffffffffu, tail);
+        const double r = student_map(sp, x, any);
+        if (i < n) t[i] = r;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_student_f32(const float *__restrict__ z, float *__restrict__ t, int64_t n, const __grid_constant__ StudentParams sp)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_round = (n + 31) / 32 * 32;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+        const double x = (i < n) ? (double)z[i] : 0.0;
+        const bool tail = !(fabs(x) < sp.zstar);
+        const bool any = __any_sync(0xffffffffu, tail);
+        const double r = student_map(sp, x, any);
+        if (i < n) t[i] = (float)r;
+    }
+}
+
+}  // namespace qm

@@ -1,0 +1,139 @@
+"""Python binding of libqm.so -- argument marshalling only.
+
+Each function has the name of the C entry point it calls (include/qm.h) and
+takes torch tensors: CUDA tensors for the device entry points, CPU tensors for
+qm_normal_quantile_host.  Outputs are allocated with torch when not given.
+PyTorch is used for device memory and streams only; every element is computed
+by the sm_100a kernels in csrc/.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+BREAKLESS, BREAKLESS77, AS241, ACKLAM, ACKLAM_REFINED = (
+    L.QM_BREAKLESS, L.QM_BREAKLESS77, L.QM_AS241, L.QM_ACKLAM, L.QM_ACKLAM_REFINED)
+
+
+def _prec(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return L.QM_F32
+    if t.dtype == torch.float64:
+        return L.QM_F64
+    raise TypeError(f"unsupported dtype {t.dtype} (float32 or float64)")
+
+
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _out(x: torch.Tensor, out, numel: int | None = None, dtype=None) -> torch.Tensor:
+    n = x.numel() if numel is None else numel
+    if out is None:
+        return torch.empty(n, dtype=dtype or x.dtype, device=x.device)
+    _dev(out, "out")
+    if out.numel() != n or out.dtype != (dtype or x.dtype):
+        raise ValueError("out has the wrong size or dtype")
+    return out
+
+
+def qm_normal_quantile(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
+    _dev(u, "u")
+    z = _out(u, out)
+    L.check("qm_normal_quantile", L.load().qm_normal_quantile(
+        u.data_ptr(), z.data_ptr(), u.numel(), _prec(u), alg, _stream(stream)))
+    return z
+
+
+def qm_normal_antithetic(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
+    _dev(u, "u")
+    z = _out(u, out, 2 * u.numel())
+    L.check("qm_normal_antithetic", L.load().qm_normal_antithetic(
+        u.data_ptr(), z.data_ptr(), u.numel(), _prec(u), alg, _stream(stream)))
+    return z
+
+
+def qm_philox_uniform(n: int, seed: int, counter_offset: int = 0, dtype=torch.float32,
+                      out=None, device=None, stream=None) -> torch.Tensor:
+    u = out if out is not None else torch.empty(n, dtype=dtype, device=device or "cuda")
+    _dev(u, "out")
+    L.check("qm_philox_uniform", L.load().qm_philox_uniform(
+        u.data_ptr(), n, _prec(u), seed, counter_offset, _stream(stream)))
+    return u
+
+
+def qm_normal_philox(n: int, seed: int, counter_offset: int = 0, dtype=torch.float32, alg: int = BREAKLESS,
+                     out=None, device=None, stream=None) -> torch.Tensor:
+    z = out if out is not None else torch.empty(n, dtype=dtype, device=device or "cuda")
+    _dev(z, "out")
+    L.check("qm_normal_philox", L.load().qm_normal_philox(
+        z.data_ptr(), n, _prec(z), alg, seed, counter_offset, _stream(stream)))
+    return z
+
+
+def qm_recycle_normal_to_t(z: torch.Tensor, nu: float, K: int = 16, zstar: float = 0.0,
+                           out=None, stream=None) -> torch.Tensor:
+    _dev(z, "z")
+    t = _out(z, out)
+    L.check("qm_recycle_normal_to_t", L.load().qm_recycle_normal_to_t(
+        z.data_ptr(), t.data_ptr(), z.numel(), _prec(z), float(nu), int(K), float(zstar), _stream(stream)))
+    return t
+
+
+def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
+    _dev(v, "v")
+    z = _out(v, out)
+    L.check("qm_recycle_exp_to_normal", L.load().qm_recycle_exp_to_normal(
+        v.data_ptr(), z.data_ptr(), v.numel(), _prec(v), alg, _stream(stream)))
+    return z
+
+
+def qm_moments(x: torch.Tensor, kmax: int = 4, workspace=None, stream=None) -> torch.Tensor:
+    """Returns the device workspace; S_k is workspace[k-1] (fp64)."""
+    _dev(x, "x")
+    ws = workspace if workspace is not None else torch.empty(L.QM_MOMENTS_WORKSPACE, dtype=torch.float64,
+                                                            device=x.device)
+    L.check("qm_moments", L.load().qm_moments(x.data_ptr(), x.numel(), _prec(x), kmax, ws.data_ptr(),
+                                              _stream(stream)))
+    return ws
+
+
+def qm_normal_quantile_host(u: torch.Tensor, out=None, alg: int = BREAKLESS) -> torch.Tensor:
+    """Host buffers in and out; the copies and the kernels run inside the call."""
+    if u.is_cuda or not u.is_contiguous():
+        raise ValueError("u must be a contiguous CPU tensor")
+    z = out if out is not None else torch.empty_like(u)
+    if z.is_cuda or z.numel() != u.numel() or z.dtype != u.dtype:
+        raise ValueError("out must be a CPU tensor like u")
+    L.check("qm_normal_quantile_host", L.load().qm_normal_quantile_host(
+        u.data_ptr(), z.data_ptr(), u.numel(), _prec(u), alg))
+    return z
+
+
+def qm_student_coefficients(nu: float, K: int):
+    import ctypes
+    import numpy as np
+    c = np.zeros(K + 1, np.float64)
+    rc = L.load().qm_student_coefficients(float(nu), int(K), c.ctypes.data_as(ctypes.c_void_p))
+    if rc != 0:
+        raise ValueError("unsupported nu/K")
+    return c
+
+
+def qm_abi_version() -> int:
+    return L.load().qm_abi_version()
+
+
+def qm_device_sm_count() -> int:
+    return L.load().qm_device_sm_count()

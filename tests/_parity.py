@@ -1,0 +1,32 @@
+"""ULP comparison of a GPU result with the oracle's long-double value (no method arithmetic)."""
+import numpy as np
+
+
+def ulp_errors(got: np.ndarray, ref_ld: np.ndarray, dtype) -> np.ndarray:
+    """|got - ref| in ulps of ref rounded to `dtype`; specials must match exactly
+    (inf with the same sign, NaN with NaN, zero with the same sign) -> 0, else inf."""
+    got = np.asarray(got, dtype=dtype)
+    ref_ld = np.asarray(ref_ld, dtype=np.longdouble)
+    ref_t = ref_ld.astype(dtype)
+    err = np.zeros(got.shape, dtype=np.float64)
+    fin = np.isfinite(ref_ld) & (ref_t != 0)
+    spacing = np.spacing(np.abs(ref_t[fin])).astype(np.longdouble)
+    err[fin] = (np.abs(got[fin].astype(np.longdouble) - ref_ld[fin]) / spacing).astype(np.float64)
+    nan_ref = np.isnan(ref_ld)
+    err[nan_ref] = np.where(np.isnan(got[nan_ref]), 0.0, np.inf)
+    inf_ref = np.isinf(ref_ld)
+    err[inf_ref] = np.where(got[inf_ref] == ref_t[inf_ref], 0.0, np.inf)
+    zero_ref = (ref_t == 0) & ~nan_ref
+    ok0 = (got[zero_ref] == 0) & (np.signbit(got[zero_ref]) == np.signbit(ref_t[zero_ref]))
+    # a nonzero ref that rounds to 0 in the target type is compared absolutely
+    tiny = zero_ref & (ref_ld != 0)
+    err[zero_ref] = np.where(ok0, 0.0, np.inf)
+    if np.any(tiny):
+        err[tiny] = np.where(np.abs(got[tiny].astype(np.longdouble) - ref_ld[tiny]) <=
+                             np.finfo(dtype).smallest_subnormal, 0.0, np.inf)
+    return err
+
+
+def summary(err: np.ndarray) -> dict:
+    h = np.histogram(np.minimum(err, 8.0), bins=[0, 0.5, 1, 1.5, 2, 3, 4, 8, 9])[0]
+    return {"max_ulp": float(err.max()) if err.size else 0.0, "hist": h.tolist()}

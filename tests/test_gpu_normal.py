@@ -1,0 +1,201 @@
+"""GPU parity of the normal-quantile hot path against the oracle (SURVEY §8 rows
+a1-a5, a7): every CUDA result is compared element by element with the oracle's
+long-double evaluation of the same formula; bar: 4 ulp (fp32), 2 ulp (fp64)
+(north star).  Calls go through the C ABI (libqm.so via the ctypes binding)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import inputs as I
+from _parity import summary, ulp_errors
+
+pytestmark = pytest.mark.gpu
+
+Q = pytest.importorskip("paper_0901_0638_b200")
+SEED = 0x5EEDC0FFEE123457
+
+CASES = [  # dtype, alg, oracle formula, coefficient precision, ulp bar
+    (np.float32, Q.BREAKLESS, O.C55, 32, 4.0),
+    (np.float32, Q.BREAKLESS77, O.A77, 32, 4.0),
+    (np.float64, Q.BREAKLESS, O.D13, 64, 2.0),
+    (np.float64, Q.BREAKLESS77, O.A77, 64, 2.0),
+]
+
+
+def _gpu(fn, x_np, **kw):
+    x = torch.from_numpy(np.ascontiguousarray(x_np)).cuda()
+    return fn(x, **kw).cpu().numpy()
+
+
+@pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
+def test_normal_quantile_mixed_inputs(dtype, alg, formula, prec, bar):
+    """2^20 + 37 inputs: odd-grid uniforms, log-uniform tails, edge values (0, 1, 1/2,
+    subnormals, NaN, out of range); several chunks of every warp and a ragged tail."""
+    u = I.mixed_uniforms((1 << 20) + 37, dtype=dtype)
+    g = _gpu(Q.qm_normal_quantile, u, alg=alg)
+    ref = O.normal_breakless(u.astype(np.float64), formula, prec)
+    err = ulp_errors(g, ref, dtype)
+    assert err.max() <= bar, summary(err)
+
+
+def test_fp32_breakless_exhaustive_grid():
+    """Every point of the fp32 odd grid (2^23 values of min(u, 1-u)), both halves."""
+    k = np.arange(1 << 23, dtype=np.float64)
+    lo = np.ldexp(2 * k + 1, -24).astype(np.float32)          # (0, 1/2)
+    u = np.concatenate([lo, (1 - lo.astype(np.float64)).astype(np.float32)])
+    g = _gpu(Q.qm_normal_quantile, u, alg=Q.BREAKLESS)
+    ref = O.normal_breakless(u.astype(np.float64), O.C55, 32)
+    err = ulp_errors(g, ref, np.float32)
+    assert err.max() <= 4.0, summary(err)
+    # odd symmetry is exact: z(1-u) = -z(u)
+    n = lo.size
+    assert np.array_equal(g[n:], -g[:n])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [0, 1, 3, 5, 63, 4097])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_ragged_and_misaligned(dtype, n, offset):
+    u = I.mixed_uniforms(n + offset + 64, dtype=dtype)[:n + offset]
+    x = torch.from_numpy(u).cuda()[offset:]                   # offset 1: not 16-byte aligned
+    out = torch.empty(n + 1, dtype=x.dtype, device="cuda")[1:] if offset else None
+    g = Q.qm_normal_quantile(x, out=out).cpu().numpy()
+    ref = O.normal_breakless(u[offset:].astype(np.float64), O.C55 if dtype == np.float32 else O.D13,
+                             32 if dtype == np.float32 else 64)
+    assert ulp_errors(g, ref, dtype).max() <= (4.0 if dtype == np.float32 else 2.0)
+
+
+def test_in_place():
+    u = I.mixed_uniforms(10000, dtype=np.float32)
+    x = torch.from_numpy(u).cuda()
+    ref = Q.qm_normal_quantile(x.clone()).cpu().numpy()
+    Q.qm_normal_quantile(x, out=x)
+    assert np.array_equal(x.cpu().numpy(), ref, equal_nan=True)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_philox_uniform_bit_exact(dtype):
+    """Raw Philox stream bit-exact vs the oracle, including a counter offset and a ragged n."""
+    n, c0 = (1 << 20) + 3, 123456789
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    g = Q.qm_philox_uniform(n, SEED, c0, dtype=tdt).cpu().numpy()
+    ref = O.philox_uniform(n, SEED, c0, dtype)
+    assert np.array_equal(g.view(np.uint32 if dtype == np.float32 else np.uint64),
+                          ref.view(np.uint32 if dtype == np.float32 else np.uint64))
+
+
+@pytest.mark.parametrize("dtype,alg", [(np.float32, Q.BREAKLESS), (np.float64, Q.BREAKLESS), (np.float32, Q.BREAKLESS77)])
+def test_fused_equals_unfused_bitwise(dtype, alg):
+    n, c0 = (1 << 20) + 5, 99
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    fused = Q.qm_normal_philox(n, SEED, c0, dtype=tdt, alg=alg)
+    u = Q.qm_philox_uniform(n, SEED, c0, dtype=tdt)
+    unf = Q.qm_normal_quantile(u, alg=alg)
+    assert torch.equal(fused, unf)
+
+
+def test_shards_concatenate_to_one_stream():
+    """Counter-offset sharding (SURVEY §8 e): rank r of G generates blocks
+    [r B, (r+1) B); the concatenation equals the single-GPU stream."""
+    n, G = 1 << 20, 4
+    whole = Q.qm_normal_philox(n, SEED, 0)
+    parts = [Q.qm_normal_philox(n // G, SEED, r * (n // G) // 4) for r in range(G)]
+    assert torch.equal(torch.cat(parts), whole)
+
+
+@pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
+def test_antithetic(dtype, alg, formula, prec, bar):
+    u = np.concatenate([I.uniform_grid(50000, dtype=dtype), I.edge_values(dtype)])
+    g = _gpu(Q.qm_normal_antithetic, u, alg=alg)
+    ref = O.normal_antithetic(u.astype(np.float64), formula, prec)
+    err = ulp_errors(g, ref, dtype)
+    assert err.max() <= bar, summary(err)
+
+
+@pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
+def test_exp_to_normal(dtype, alg, formula, prec, bar):
+    big = [1e3, -1e6, 3e12, -1e30, 1e300] if dtype == np.float64 else [1e3, -1e6, 3e12, -1e30]
+    v = np.concatenate([I.laplace(100000, dtype=dtype),
+                        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 37.0, -74.0, 1e-30] + big, dtype=dtype)])
+    g = _gpu(Q.qm_recycle_exp_to_normal, v, alg=alg)
+    ref = O.exp_to_normal(v.astype(np.float64), formula, prec)
+    err = ulp_errors(g, ref, dtype)
+    assert err.max() <= bar, summary(err)
+
+
+# -------------------------------------------------- comparison quantiles (a5)
+@pytest.mark.parametrize("alg,name", [(Q.AS241, "as241"), (Q.ACKLAM, "acklam")])
+def test_branchy_baselines(alg, name):
+    u = I.mixed_uniforms((1 << 18) + 11, dtype=np.float64)
+    g = _gpu(Q.qm_normal_quantile, u, alg=alg)
+    ref = O.normal_as241(u.astype(np.float64), 64) if name == "as241" else O.normal_acklam(u, 64, False)
+    err = ulp_errors(g, ref, np.float64)
+    assert err.max() <= 2.0, summary(err)
+
+
+def test_refined_acklam():
+    """Refined Acklam: the Halley step forms Phi(x) - t in double (as published), so
+    near the centre its error is |d(Phi - t)|/phi(x) ~ 8 eps t / phi(x) -- the
+    paper's 'loss of precision in the middle'.  Bar: 2 ulp + that term."""
+    u = I.mixed_uniforms((1 << 18) + 11, dtype=np.float64)
+    g = _gpu(Q.qm_normal_quantile, u, alg=Q.ACKLAM_REFINED)
+    ref = O.normal_acklam(u, 64, True)
+    fin = np.isfinite(ref)
+    r = ref[fin].astype(np.float64)
+    t = np.minimum(u[fin], 1 - u[fin])
+    phi = np.exp(-0.5 * r * r) / np.sqrt(2 * np.pi)
+    tol = 2 * np.spacing(np.abs(r)) + 8 * np.finfo(np.float64).eps * t / phi
+    assert np.all(np.abs(g[fin] - r) <= tol)
+    assert np.array_equal(np.isnan(g), np.isnan(ref.astype(np.float64)))
+
+
+# --------------------------------------- full size, bench launch configuration
+def test_full_size_streaming_sampled():
+    """configs[1]: 2^28 fp32 uniforms in HBM -> breakless quantile (the bench.py
+    launch); 2^20 sampled outputs checked against the oracle one by one."""
+    n = 1 << 28
+    u = Q.qm_philox_uniform(n, SEED, 0)
+    z = Q.qm_normal_quantile(u)
+    idx = np.sort(np.random.default_rng(1).choice(n, 1 << 20, replace=False))
+    ti = torch.from_numpy(idx).cuda()
+    us, zs = u[ti].cpu().numpy(), z[ti].cpu().numpy()
+    assert np.array_equal(us, O.philox_uniform_at(idx, SEED, 0, np.float32))
+    err = ulp_errors(zs, O.normal_breakless(us.astype(np.float64), O.C55, 32), np.float32)
+    assert err.max() <= 4.0, summary(err)
+    # whole-array properties: finite, |z| < 5.4 on the fp32 grid, sign matches u - 1/2
+    assert bool(torch.isfinite(z).all()) and float(z.abs().max()) < 5.4
+    assert int((z > 0).sum()) == int((u > 0.5).sum())
+    del u, z
+
+
+def test_full_size_fused_sampled():
+    """configs[2]: Philox-fused 2^32 fp32 normal samples; sampled parity."""
+    n = 1 << 32
+    z = Q.qm_normal_philox(n, SEED, 0)
+    idx = np.sort(np.random.default_rng(2).choice(n, 1 << 18, replace=False))
+    zs = z[torch.from_numpy(idx).cuda()].cpu().numpy()
+    us = O.philox_uniform_at(idx, SEED, 0, np.float32)
+    err = ulp_errors(zs, O.normal_breakless(us.astype(np.float64), O.C55, 32), np.float32)
+    assert err.max() <= 4.0, summary(err)
+    m = z.double().mean().item()
+    assert abs(m) < 6 / np.sqrt(n) * 10
+    del z
+
+
+def test_host_entry_point_equals_device():
+    """The e2e C-ABI call on host buffers gives the device path's bits."""
+    u = I.mixed_uniforms((1 << 22) + 7, dtype=np.float32)
+    dev = _gpu(Q.qm_normal_quantile, u)
+    host = Q.qm_normal_quantile_host(torch.from_numpy(u)).numpy()
+    assert np.array_equal(dev, host, equal_nan=True)
+    u64 = I.mixed_uniforms((1 << 20) + 7, dtype=np.float64)
+    assert np.array_equal(_gpu(Q.qm_normal_quantile, u64),
+                          Q.qm_normal_quantile_host(torch.from_numpy(u64)).numpy(), equal_nan=True)
+
+
+def test_determinism_across_launches():
+    u = torch.from_numpy(I.mixed_uniforms(1 << 20, dtype=np.float64)).cuda()
+    a = Q.qm_normal_quantile(u)
+    b = Q.qm_normal_quantile(u)
+    assert torch.equal(a.nan_to_num(), b.nan_to_num())

@@ -1,0 +1,44 @@
+"""Launch one hot-path kernel a few times (for ncu).  python tools/prof_kernel.py <name> [reps]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_0901_0638_b200 as Q  # noqa: E402
+
+SEED = 0x5EEDC0FFEE123457
+name = sys.argv[1] if len(sys.argv) > 1 else "stream_f32"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+n = 1 << 28
+if name == "stream_f32":
+    u = Q.qm_philox_uniform(n, SEED, 0)
+    z = torch.empty_like(u)
+    fn = lambda: Q.qm_normal_quantile(u, out=z)
+elif name == "stream_f64":
+    u = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
+    z = torch.empty_like(u)
+    fn = lambda: Q.qm_normal_quantile(u, out=z)
+elif name == "fused_f32":
+    z = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
+    fn = lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=z)
+elif name == "fused_f64":
+    z = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_normal_philox(1 << 31, SEED, 0, dtype=torch.float64, out=z)
+elif name.startswith("config1_"):
+    import numpy as np
+    from synth import inputs as I
+    alg = {"breakless": Q.BREAKLESS, "as241": Q.AS241, "acklam": Q.ACKLAM, "refined": Q.ACKLAM_REFINED}[name[8:]]
+    u = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
+    z = torch.empty_like(u)
+    fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
+elif name == "student":
+    zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
+    t = torch.empty_like(zn)
+    fn = lambda: Q.qm_recycle_normal_to_t(zn, 4.0, 10, 3.93473, out=t)
+else:
+    raise SystemExit(f"unknown {name}")
+for _ in range(reps):
+    fn()
+torch.cuda.synchronize()
+print("done", name)
