@@ -216,7 +216,7 @@ int orc_normal_antithetic(const double *u, ld *out, int64_t n, int formula, int 
         ld ui = (ld)u[i], z;
         if (isnan(ui) || ui < 0.0L || ui > 1.0L) z = NAN;
         else if (ui == 0.0L) z = INFINITY;
-        else z = rational_Q(&r, -logl(ui));
+        else z = rational_Q(&r, 0.0L - logl(ui));   /* v = -log u >= 0, +0 at u = 1 (Z >= 0) */
         out[2 * i] = z;
         out[2 * i + 1] = -z;
     }

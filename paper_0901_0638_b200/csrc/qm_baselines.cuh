@@ -67,7 +67,7 @@ QM_DEV double as241(double u)
         return dd_div_round(num, horner_dd<8>(kAS_B, r));
     }
     const double t = (qd < 0.0) ? u : __dadd_rn(1.0, -u);         // exact
-    const dd R = dd_sqrt(neg_log2x_dd(t, -1));                     // sqrt(-log t)
+    const dd R = dd_sqrt(neg_log_dd(t));                           // sqrt(-log t)
     double x;
     if (R.hi <= 5.0) {
         const dd r = dd_add_d(R, -1.6);
@@ -83,7 +83,7 @@ QM_DEV double as241(double u)
 QM_DEV double acklam_lower(double t)
 {
     if (t < 0.02425) {
-        const dd L = neg_log2x_dd(t, -1);                          // -log t
+        const dd L = neg_log_dd(t);                                 // -log t
         const dd q = dd_sqrt(dd{2.0 * L.hi, 2.0 * L.lo});
         return dd_div_round(horner_dd<6>(kAK_C, q), horner_dd<5>(kAK_D, q));
     }

@@ -103,10 +103,17 @@ QM_DEV dd dd_exp(dd x)
     return dd{s.hi * sc, s.lo * sc};
 }
 
-// natural log of a positive normal double as dd
+// -log(x) as dd for any positive finite x (subnormals pre-scaled by 2^54)
+QM_DEV dd neg_log_dd(double x)
+{
+    const bool sub = x < 2.2250738585072014e-308;
+    return neg_log2x_dd(sub ? __dmul_rn(x, 18014398509481984.0) : x, sub ? -55 : -1);
+}
+
+// natural log of a positive finite double as dd
 QM_DEV dd dd_log(double x)
 {
-    const dd m = neg_log2x_dd(x, -1);                  // -log(x)
+    const dd m = neg_log_dd(x);
     return dd{-m.hi, -m.lo};
 }
 

@@ -14,6 +14,7 @@
 //    scalar code in the same launch.
 #pragma once
 #include "qm_math.cuh"
+#include "qm_tma.cuh"
 
 namespace qm {
 
@@ -70,6 +71,51 @@ k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int 
     if (i < n) z[i] = nq_f32_careful<ALG>(u[i]);
     for (int64_t j = i + (int64_t)gridDim.x * blockDim.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
         z[j] = nq_f32_careful<ALG>(u[j]);
+}
+
+// ------------------------------------------------- fp32 normal, TMA pipeline
+constexpr int kTmaTile = 8192;            // floats per tile (32 KB)
+constexpr int kTmaStages = 4;             // 128 KB of shared memory per SM
+constexpr int kTmaNC = 16;                // consumer warps (+1 producer warp)
+constexpr int kTmaThreads = 32 * (kTmaNC + 1);
+
+template <int ALG>
+struct OpNormalF32 {
+    QM_DEV void tile(float *t, int ctid, int nct) const
+    {
+        float4 *t4 = reinterpret_cast<float4 *>(t);
+        const int per = kTmaTile / 4 / (kTmaNC * 32);
+#pragma unroll 2
+        for (int j = 0; j < per; ++j) {
+            float4 *p = t4 + ctid + j * nct;
+            const float4 a = *p;
+            const float x[4] = {a.x, a.y, a.z, a.w};
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= 1.17549435e-38f);
+            float y[4];
+            if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+                for (int k = 0; k < 4; k += 2) {
+                    const float oa = __fsub_rn(1.0f, x[k]), ob = __fsub_rn(1.0f, x[k + 1]);
+                    const float2 lz = neg_log2x_f32x2(fminf(x[k], oa), fminf(x[k + 1], ob));
+                    y[k] = apply_sign_f32(rat32<ALG>(lz.x), x[k], oa);
+                    y[k + 1] = apply_sign_f32(rat32<ALG>(lz.y), x[k + 1], ob);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
+            }
+            *p = make_float4(y[0], y[1], y[2], y[3]);
+        }
+    }
+};
+
+template <int ALG>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_normal_f32_tma(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
+{
+    tma_stream_map<float, kTmaTile, kTmaStages, kTmaNC>(u, z, ntiles, OpNormalF32<ALG>{});
 }
 
 // ------------------------------------------------------------ fp64 normal
@@ -301,6 +347,28 @@ k_exp2n_f32(const float *__restrict__ v, float *__restrict__ z, int64_t n, int v
     }
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t j = 4 * nv + t; j < n; j += (int64_t)gridDim.x * blockDim.x) z[j] = exp2n_f32<ALG>(v[j]);
+}
+
+template <int ALG>
+struct OpExp2nF32 {
+    QM_DEV void tile(float *t, int ctid, int nct) const
+    {
+        float4 *t4 = reinterpret_cast<float4 *>(t);
+        const int per = kTmaTile / 4 / (kTmaNC * 32);
+#pragma unroll 2
+        for (int j = 0; j < per; ++j) {
+            float4 *p = t4 + ctid + j * nct;
+            const float4 a = *p;
+            *p = make_float4(exp2n_f32<ALG>(a.x), exp2n_f32<ALG>(a.y), exp2n_f32<ALG>(a.z), exp2n_f32<ALG>(a.w));
+        }
+    }
+};
+
+template <int ALG>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_exp2n_f32_tma(const float *__restrict__ v, float *__restrict__ z, int64_t ntiles)
+{
+    tma_stream_map<float, kTmaTile, kTmaStages, kTmaNC>(v, z, ntiles, OpExp2nF32<ALG>{});
 }
 
 // fp64: for |v| >= 2^40 the polynomials would overflow in double; evaluate the

@@ -53,6 +53,42 @@ qm_status launched()
 
 bool bad_ptrs(const void *a, const void *b, int64_t n) { return n > 0 && (a == nullptr || b == nullptr); }
 
+// QM_STREAM_PATH=ldg forces the register-pipelined LDG kernels (A/B diagnostics)
+bool tma_enabled()
+{
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("QM_STREAM_PATH");
+        on = (e && strcmp(e, "ldg") == 0) ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// fp32 elementwise map: whole 32 KB tiles through the TMA pipeline (one
+// persistent CTA per SM), the remainder (< 1 tile) and misaligned arrays
+// through the LDG kernel.
+template <typename KT, typename KL>
+qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64_t n, cudaStream_t s)
+{
+    const int vec = aligned16(in) && aligned16(out);
+    int64_t ntiles = (vec && tma_enabled()) ? n / kTmaTile : 0;
+    if (ntiles > 0) {
+        const size_t smem = (size_t)kTmaStages * kTmaTile * sizeof(float);
+        if (cudaFuncSetAttribute(ktma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return QM_ECUDA;
+        const int sms = sm_count_for_current_device();
+        int64_t g = sms > 0 ? sms : 148;
+        if (ntiles < g) g = ntiles;
+        ktma<<<(int)g, kTmaThreads, smem, s>>>(in, out, ntiles);
+    }
+    const int64_t done = ntiles * kTmaTile, rest = n - done;
+    if (rest > 0) {
+        const int g = grid_for(rest, kThreads * 8, 8);
+        kldg<<<g, kThreads, 0, s>>>(in + done, out + done, rest, vec);
+    }
+    return launched();
+}
+
 }  // namespace
 
 extern "C" {
@@ -82,12 +118,11 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     const int vec = aligned16(u) && aligned16(z);
     if (p == QM_F32) {
         if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
-        const int g = grid_for(n, kThreads * 8, 8);
         if (alg == QM_BREAKLESS)
-            k_normal_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
-        else
-            k_normal_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
-        return launched();
+            return launch_stream_f32(k_normal_f32_tma<ALG_BREAKLESS>, k_normal_f32<ALG_BREAKLESS>,
+                                     (const float *)u, (float *)z, n, s);
+        return launch_stream_f32(k_normal_f32_tma<ALG_BREAKLESS77>, k_normal_f32<ALG_BREAKLESS77>,
+                                 (const float *)u, (float *)z, n, s);
     }
     const int g = grid_for(n, kThreads * 4, 8);
     switch (alg) {
@@ -173,12 +208,11 @@ qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precisi
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     if (p == QM_F32) {
-        const int vec = aligned16(v) && aligned16(z);
-        const int g = grid_for(n, kThreads * 8, 8);
         if (alg == QM_BREAKLESS)
-            k_exp2n_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)v, (float *)z, n, vec);
-        else
-            k_exp2n_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)v, (float *)z, n, vec);
+            return launch_stream_f32(k_exp2n_f32_tma<ALG_BREAKLESS>, k_exp2n_f32<ALG_BREAKLESS>,
+                                     (const float *)v, (float *)z, n, s);
+        return launch_stream_f32(k_exp2n_f32_tma<ALG_BREAKLESS77>, k_exp2n_f32<ALG_BREAKLESS77>,
+                                 (const float *)v, (float *)z, n, s);
     } else {
         const int g = grid_for(n, kThreads, 8);
         if (alg == QM_BREAKLESS)

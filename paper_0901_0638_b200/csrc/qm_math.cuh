@@ -16,7 +16,9 @@
 //    the last K steps of P and Q, a double-double quotient and one final
 //    rounding: <= ~0.7 ulp.
 #pragma once
+#ifndef QM_PRIM_EXTERNAL   // (a development-time CPU emulation supplies its own primitives)
 #include "qm_prim.cuh"
+#endif
 
 namespace qm {
 
@@ -185,10 +187,13 @@ QM_DEV dd neg_log2x_dd(double vv, int eadj)
     const double dl = __dadd_rn(f, -__dadd_rn(dh, -2.0));   // Fast2Sum, |2| >= |f|
     double r = rcp_approx_f64(dh);
     r = __fma_rn(r, __fma_rn(-dh, r, 1.0), r);               // ~2^-44
-    const double sh = __dmul_rn(f, r);
-    double rem = __fma_rn(-sh, dh, f);
-    rem = __fma_rn(-sh, dl, rem);
-    const double sl = __dmul_rn(rem, r);
+    const double s0 = __dmul_rn(f, r);
+    double rem = __fma_rn(-s0, dh, f);
+    rem = __fma_rn(-s0, dl, rem);
+    const double s1 = __dmul_rn(rem, r);
+    // renormalise so that |sl| <= ulp(sh)/2: the cubic term below uses sh only
+    const double sh = __dadd_rn(s0, s1);
+    const double sl = __dadd_rn(s1, -__dadd_rn(sh, -s0));    // Fast2Sum, |s0| >= |s1|
     // log1p(f) = 2 sh + (2 sl + sh^3 T(sh^2))
     const double w = __dmul_rn(sh, sh);
     double T = kLogT[7];

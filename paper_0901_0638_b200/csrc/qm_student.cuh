@@ -40,19 +40,17 @@ QM_DEV double student_central(const StudentParams &sp, double a)
 QM_DEV double student_tail(const StudentParams &sp, double a)
 {
     // log w = log(erfc(a/sqrt2)) + log(C_nu/2); erfc(x) = exp(-x^2) erfcx(x)
-    const double x = a * 0.70710678118654752440;
     const double xh = __dmul_rn(a, 0.70710678118654752440);
     const double xl = __fma_rn(a, 0.70710678118654752440, -xh) + a * (-4.8336466567264567e-17);
-    (void)x;
     const dd x2 = dd_mul(dd{xh, xl}, dd{xh, xl});
     const dd lx = dd_log(erfcx(xh));
     dd logw = dd_add(dd{-x2.hi, -x2.lo}, lx);
     logw = dd_add(logw, dd{sp.logC_hi, sp.logC_lo});
     // w^(-1/nu), w^(2/nu)
-    const dd e1 = dd_exp(dd_mul_d(logw, -sp.inv_nu));
-    const dd e2 = dd_exp(dd_mul_d(logw, sp.two_over_nu));
+    const dd e1 = dd_exp(dd_mul(logw, dd{-sp.inv_nu, -sp.inv_nu_lo}));
+    const dd e2 = dd_exp(dd_mul(logw, dd{sp.two_over_nu, sp.two_over_nu_lo}));
     const dd corr = dd_add_d(dd_mul_d(e2, -sp.acoef), 1.0);
-    const dd t = dd_mul(dd_mul_d(e1, sp.sqrt_nu), corr);
+    const dd t = dd_mul(dd_mul(e1, dd{sp.sqrt_nu, sp.sqrt_nu_lo}), corr);
     return t.hi + t.lo;
 }
 

@@ -58,9 +58,9 @@ bool student_params(double nu_d, int K, double zstar, StudentParams *out)
     for (int k = 0; k <= K; ++k) sp.c[k] = (double)c[k];
     sp.K = K;
     sp.zstar = zstar;
-    sp.sqrt_nu = (double)sqrtq(n);
-    sp.inv_nu = (double)(1 / n);
-    sp.two_over_nu = (double)(2 / n);
+    split_dd(sqrtq(n), &sp.sqrt_nu, &sp.sqrt_nu_lo);
+    split_dd(1 / n, &sp.inv_nu, &sp.inv_nu_lo);
+    split_dd(2 / n, &sp.two_over_nu, &sp.two_over_nu_lo);
     sp.acoef = (double)((n + 1) / (2 * (n + 2)));
     // log(C_n / 2) = log(n) + log(pi)/2 + lg_ratio - log 2
     const __float128 logC2 = logq(n) + logq(M_PIq) / 2 + lg_ratio - logq((__float128)2);

@@ -10,7 +10,10 @@ struct StudentParams {
     double c[QM_STUDENT_KMAX + 1];   // c_0..c_K of the central series
     int K;
     double zstar;                    // crossover
-    double sqrt_nu, inv_nu, two_over_nu, acoef;     // acoef = (nu+1)/(2(nu+2))
+    // double-double constants: in the far tail log w ~ -700, so 1/nu must carry
+    // more than 53 bits for w^(-1/nu) to stay within an ulp
+    double sqrt_nu, sqrt_nu_lo, inv_nu, inv_nu_lo, two_over_nu, two_over_nu_lo;
+    double acoef;                    // (nu+1)/(2(nu+2))
     double logC_hi, logC_lo;         // log(C_nu / 2) as a double-double, C_nu = nu sqrt(pi) G(nu/2)/G((nu+1)/2)
 };
 

@@ -9,9 +9,15 @@ def ulp_errors(got: np.ndarray, ref_ld: np.ndarray, dtype) -> np.ndarray:
     ref_ld = np.asarray(ref_ld, dtype=np.longdouble)
     ref_t = ref_ld.astype(dtype)
     err = np.zeros(got.shape, dtype=np.float64)
-    fin = np.isfinite(ref_ld) & (ref_t != 0)
+    if got.size == 0:
+        return err
+    fin = np.isfinite(ref_t) & (ref_t != 0)
     spacing = np.spacing(np.abs(ref_t[fin])).astype(np.longdouble)
-    err[fin] = (np.abs(got[fin].astype(np.longdouble) - ref_ld[fin]) / spacing).astype(np.float64)
+    e = (np.abs(got[fin].astype(np.longdouble) - ref_ld[fin]) / spacing).astype(np.float64)
+    err[fin] = np.where(np.isnan(e), np.inf, e)
+    # a finite reference beyond the target type's range must round to +-inf
+    ovf = np.isfinite(ref_ld) & np.isinf(ref_t)
+    err[ovf] = np.where(got[ovf] == ref_t[ovf], 0.0, np.inf)
     nan_ref = np.isnan(ref_ld)
     err[nan_ref] = np.where(np.isnan(got[nan_ref]), 0.0, np.inf)
     inf_ref = np.isinf(ref_ld)
@@ -28,5 +34,7 @@ def ulp_errors(got: np.ndarray, ref_ld: np.ndarray, dtype) -> np.ndarray:
 
 
 def summary(err: np.ndarray) -> dict:
+    if err.size == 0:
+        return {"max_ulp": 0.0, "hist": []}
     h = np.histogram(np.minimum(err, 8.0), bins=[0, 0.5, 1, 1.5, 2, 3, 4, 8, 9])[0]
     return {"max_ulp": float(err.max()) if err.size else 0.0, "hist": h.tolist()}

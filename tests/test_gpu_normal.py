@@ -63,7 +63,8 @@ def test_ragged_and_misaligned(dtype, n, offset):
     g = Q.qm_normal_quantile(x, out=out).cpu().numpy()
     ref = O.normal_breakless(u[offset:].astype(np.float64), O.C55 if dtype == np.float32 else O.D13,
                              32 if dtype == np.float32 else 64)
-    assert ulp_errors(g, ref, dtype).max() <= (4.0 if dtype == np.float32 else 2.0)
+    e = ulp_errors(g, ref, dtype)
+    assert (e.max() if e.size else 0.0) <= (4.0 if dtype == np.float32 else 2.0)
 
 
 def test_in_place():
