@@ -413,7 +413,7 @@ static ld acklam_one(ld p, int prec, int refine)
         ld q = t - 0.5L, r = q * q;
         x = hornerA(AK_A, 6, prec, r) * q / (hornerA(AK_B, 5, prec, r) * r + 1.0L);
     }
-    if (refine) {
+    if (refine && (double)t >= 2.2250738585072014e-308) {   /* R20: the double-precision step overflows for subnormal t */
         ld e = 0.5L * erfcl(-x * SQRT1_2L) - t;
         ld uu = e * 2.50662827463100050242L * expl(0.5L * x * x);
         x = x - uu / (1.0L + 0.5L * x * uu);

@@ -100,7 +100,7 @@ QM_DEV double acklam(double p)
     if (p == 1.0) return inf_d();
     const double t = (p < 0.5) ? p : __dadd_rn(1.0, -p);
     double x = acklam_lower(t);
-    if (REFINE) {
+    if (REFINE && t >= 2.2250738585072014e-308) {   // R20: exp(x^2/2) overflows for subnormal t; keep level 1
         // Halley step of the published refinement (plain double, as published)
         const double e = 0.5 * erfc(-x * 0.70710678118654752440) - t;
         const double uu = e * 2.50662827463100050242 * exp(0.5 * x * x);

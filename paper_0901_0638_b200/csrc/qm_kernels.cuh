@@ -22,7 +22,7 @@ constexpr int kThreads = 256;
 
 // ------------------------------------------------------------ fp32 normal
 template <int ALG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
 k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int vec)
 {
     constexpr int V = 2;                                  // float4 per lane per chunk
@@ -74,18 +74,24 @@ k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int 
 }
 
 // ------------------------------------------------- fp32 normal, TMA pipeline
-constexpr int kTmaTile = 8192;            // floats per tile (32 KB)
-constexpr int kTmaStages = 4;             // 128 KB of shared memory per SM
-constexpr int kTmaNC = 16;                // consumer warps (+1 producer warp)
-constexpr int kTmaThreads = 32 * (kTmaNC + 1);
+// pipeline shapes: NC consumer warps (+1 producer), STAGES x TILE floats of
+// shared memory per CTA, MINB CTAs per SM
+template <int NC_, int STAGES_, int TILE_, int MINB_>
+struct TmaCfg {
+    static constexpr int NC = NC_, STAGES = STAGES_, TILE = TILE_, MINB = MINB_, THREADS = 32 * (NC_ + 1);
+    static_assert(TILE_ % (4 * 32 * NC_) == 0, "tile must split evenly over the consumer threads");
+};
+using TmaCfgA = TmaCfg<16, 4, 8192, 1>;   // 1 CTA/SM, 16 consumer warps, 128 KB
+using TmaCfgB = TmaCfg<16, 3, 8192, 2>;   // 2 CTAs/SM, 32 consumer warps, 2 x 96 KB
+using TmaCfgC = TmaCfg<31, 4, 7936, 1>;   // 1 CTA/SM, 31 consumer warps, 124 KB
 
-template <int ALG>
+template <int ALG, class CFG>
 struct OpNormalF32 {
     QM_DEV void tile(float *t, int ctid, int nct) const
     {
         float4 *t4 = reinterpret_cast<float4 *>(t);
-        const int per = kTmaTile / 4 / (kTmaNC * 32);
-#pragma unroll 2
+        constexpr int per = CFG::TILE / 4 / (CFG::NC * 32);
+#pragma unroll 1
         for (int j = 0; j < per; ++j) {
             float4 *p = t4 + ctid + j * nct;
             const float4 a = *p;
@@ -111,11 +117,11 @@ struct OpNormalF32 {
     }
 };
 
-template <int ALG>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
 k_normal_f32_tma(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
 {
-    tma_stream_map<float, kTmaTile, kTmaStages, kTmaNC>(u, z, ntiles, OpNormalF32<ALG>{});
+    tma_stream_map<float, CFG::TILE, CFG::STAGES, CFG::NC>(u, z, ntiles, OpNormalF32<ALG, CFG>{});
 }
 
 // ------------------------------------------------------------ fp64 normal
@@ -349,12 +355,12 @@ k_exp2n_f32(const float *__restrict__ v, float *__restrict__ z, int64_t n, int v
     for (int64_t j = 4 * nv + t; j < n; j += (int64_t)gridDim.x * blockDim.x) z[j] = exp2n_f32<ALG>(v[j]);
 }
 
-template <int ALG>
+template <int ALG, class CFG>
 struct OpExp2nF32 {
     QM_DEV void tile(float *t, int ctid, int nct) const
     {
         float4 *t4 = reinterpret_cast<float4 *>(t);
-        const int per = kTmaTile / 4 / (kTmaNC * 32);
+        constexpr int per = CFG::TILE / 4 / (CFG::NC * 32);
 #pragma unroll 2
         for (int j = 0; j < per; ++j) {
             float4 *p = t4 + ctid + j * nct;
@@ -364,11 +370,11 @@ struct OpExp2nF32 {
     }
 };
 
-template <int ALG>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
 k_exp2n_f32_tma(const float *__restrict__ v, float *__restrict__ z, int64_t ntiles)
 {
-    tma_stream_map<float, kTmaTile, kTmaStages, kTmaNC>(v, z, ntiles, OpExp2nF32<ALG>{});
+    tma_stream_map<float, CFG::TILE, CFG::STAGES, CFG::NC>(v, z, ntiles, OpExp2nF32<ALG, CFG>{});
 }
 
 // fp64: for |v| >= 2^40 the polynomials would overflow in double; evaluate the

@@ -4,6 +4,7 @@
 // configures and enqueues.
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -64,29 +65,55 @@ bool tma_enabled()
     return on == 1;
 }
 
-// fp32 elementwise map: whole 32 KB tiles through the TMA pipeline (one
-// persistent CTA per SM), the remainder (< 1 tile) and misaligned arrays
-// through the LDG kernel.
-template <typename KT, typename KL>
+// fp32 elementwise map: whole tiles through the TMA pipeline (persistent CTAs),
+// the remainder (< 1 tile) and misaligned arrays through the LDG kernel.
+template <class CFG, typename KT, typename KL>
 qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64_t n, cudaStream_t s)
 {
     const int vec = aligned16(in) && aligned16(out);
-    int64_t ntiles = (vec && tma_enabled()) ? n / kTmaTile : 0;
+    int64_t ntiles = (vec && tma_enabled()) ? n / CFG::TILE : 0;
     if (ntiles > 0) {
-        const size_t smem = (size_t)kTmaStages * kTmaTile * sizeof(float);
+        const size_t smem = (size_t)CFG::STAGES * CFG::TILE * sizeof(float);
         if (cudaFuncSetAttribute(ktma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return QM_ECUDA;
         const int sms = sm_count_for_current_device();
-        int64_t g = sms > 0 ? sms : 148;
+        int64_t g = (int64_t)(sms > 0 ? sms : 148) * CFG::MINB;
         if (ntiles < g) g = ntiles;
-        ktma<<<(int)g, kTmaThreads, smem, s>>>(in, out, ntiles);
+        ktma<<<(int)g, CFG::THREADS, smem, s>>>(in, out, ntiles);
     }
-    const int64_t done = ntiles * kTmaTile, rest = n - done;
+    const int64_t done = ntiles * CFG::TILE, rest = n - done;
     if (rest > 0) {
         const int g = grid_for(rest, kThreads * 8, 8);
         kldg<<<g, kThreads, 0, s>>>(in + done, out + done, rest, vec);
     }
     return launched();
+}
+
+// QM_TMA_CFG=A|B|C selects the pipeline shape (A/B diagnostics; default B)
+char tma_cfg()
+{
+    static char c = 0;
+    if (!c) {
+        const char *e = getenv("QM_TMA_CFG");
+        c = (e && (e[0] == 'A' || e[0] == 'B' || e[0] == 'C')) ? e[0] : 'B';
+    }
+    return c;
+}
+
+template <int ALG>
+qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
+{
+    switch (tma_cfg()) {
+    case 'A': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
+    case 'C': return launch_stream_f32<TmaCfgC>(k_normal_f32_tma<ALG, TmaCfgC>, k_normal_f32<ALG>, u, z, n, s);
+    default: return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
+    }
+}
+
+template <int ALG>
+qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
+{
+    return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
 }
 
 }  // namespace
@@ -118,11 +145,8 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     const int vec = aligned16(u) && aligned16(z);
     if (p == QM_F32) {
         if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
-        if (alg == QM_BREAKLESS)
-            return launch_stream_f32(k_normal_f32_tma<ALG_BREAKLESS>, k_normal_f32<ALG_BREAKLESS>,
-                                     (const float *)u, (float *)z, n, s);
-        return launch_stream_f32(k_normal_f32_tma<ALG_BREAKLESS77>, k_normal_f32<ALG_BREAKLESS77>,
-                                 (const float *)u, (float *)z, n, s);
+        if (alg == QM_BREAKLESS) return normal_f32<ALG_BREAKLESS>((const float *)u, (float *)z, n, s);
+        return normal_f32<ALG_BREAKLESS77>((const float *)u, (float *)z, n, s);
     }
     const int g = grid_for(n, kThreads * 4, 8);
     switch (alg) {
@@ -208,11 +232,8 @@ qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precisi
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     if (p == QM_F32) {
-        if (alg == QM_BREAKLESS)
-            return launch_stream_f32(k_exp2n_f32_tma<ALG_BREAKLESS>, k_exp2n_f32<ALG_BREAKLESS>,
-                                     (const float *)v, (float *)z, n, s);
-        return launch_stream_f32(k_exp2n_f32_tma<ALG_BREAKLESS77>, k_exp2n_f32<ALG_BREAKLESS77>,
-                                 (const float *)v, (float *)z, n, s);
+        if (alg == QM_BREAKLESS) return exp2n_f32<ALG_BREAKLESS>((const float *)v, (float *)z, n, s);
+        return exp2n_f32<ALG_BREAKLESS77>((const float *)v, (float *)z, n, s);
     } else {
         const int g = grid_for(n, kThreads, 8);
         if (alg == QM_BREAKLESS)
