@@ -218,8 +218,8 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     for nu, K, zs in [(4.0, 10, 3.93473), (3.0, 16, 3.5667), (5.0, 16, 4.6506), (10.0, 16, 6.9584)]:
         rec(f"student_f64_nu{int(nu)}_K{K}_2^30",
             lambda nu=nu, K=K, zs=zs: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=tt), 1 << 30, 16)
-    ws = torch.empty(4 + 4 * 1024, dtype=torch.float64, device="cuda")
-    rec("moments_f64_2^30", lambda: Q.qm_moments(tt, 4, workspace=ws), 1 << 30, 8)
+    ws = torch.empty(4 * Q.qm_moment_row_count(1 << 30), dtype=torch.float64, device="cuda")
+    rec("moments_f64_2^30", lambda: Q.qm_moments(tt, 4, rows=ws), 1 << 30, 8)
     del zn, tt
     # config 5 building block: Laplace -> normal
     from synth import inputs as I

@@ -110,14 +110,24 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
 qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precision p,
                                    qm_algorithm alg, void *stream);
 
-/* Moment sums S_k = sum_i x_i^k, k = 1..kmax (kmax <= 4), accumulated in fp64
- * in a fixed order independent of the launch and the device (row a8).
- * sums_dev is a caller-owned device array of QM_MOMENTS_WORKSPACE doubles:
- * S_k is written to sums_dev[k-1], the rest is scratch.  Two calls must not
- * share a workspace concurrently. */
-#define QM_MOMENTS_WORKSPACE (4 + 4 * 1024)
+/* Moment sums S_k = sum_i x_i^k, k = 1..4 (row a8; the north star's "moment
+ * ... sums" that the multi-GPU harness all-reduces).  Deterministic for any
+ * launch, device and DEVICE COUNT:
+ *  - qm_moment_rows: the array is cut into fixed chunks of QM_MOMENT_CHUNK
+ *    elements; rows[4r + k-1] = sum over chunk r of x^k, in a fixed order.
+ *    rows has qm_moment_row_count(n) * 4 doubles (caller-owned, device).
+ *  - qm_reduce_rows: out[c] = sum over r of rows[r * ncol + c] in a fixed tree
+ *    (1 <= ncol <= 64).  A rank owning chunks [c0, c1) of a global stream
+ *    writes rows [c0, c1) of a zeroed global matrix; an all-reduce(SUM) of the
+ *    matrix is exact and qm_reduce_rows gives the same bits for 1 or 8 GPUs.
+ *  - qm_moments = both, S_k in sums_dev[k-1] (kmax <= 4 written), rows_ws as
+ *    for qm_moment_rows. */
+#define QM_MOMENT_CHUNK 65536
+int64_t   qm_moment_row_count(int64_t n);
+qm_status qm_moment_rows(const void *x, int64_t n, qm_precision p, double *rows, void *stream);
+qm_status qm_reduce_rows(const double *rows, int64_t nrows, int ncol, double *out, void *stream);
 qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax,
-                     double *sums_dev, void *stream);
+                     double *sums_dev, double *rows_ws, void *stream);
 
 /* End-to-end variant of qm_normal_quantile on HOST buffers: copies u in,
  * computes, copies z out, overlapping the three in chunks on library-owned

@@ -2,9 +2,10 @@
 arXiv 0901.0638): the C ABI of libqm.so (include/qm.h) and its Python binding.
 
 The package holds only the hot path: csrc/ (sm_100a kernels + C ABI),
-qm.py (binding, same names as the C entry points), build.py (nvcc build).
+qm.py (binding, same names as the C entry points), shard.py (multi-GPU
+sharding + the all-reduce of sums), build.py (nvcc build).
 """
 from .qm import (  # noqa: F401
-    ACKLAM, ACKLAM_REFINED, AS241, BREAKLESS, BREAKLESS77, qm_abi_version, qm_device_sm_count, qm_moments,
-    qm_normal_antithetic, qm_normal_philox, qm_normal_quantile, qm_normal_quantile_host, qm_philox_uniform,
-    qm_recycle_exp_to_normal, qm_recycle_normal_to_t, qm_student_coefficients)
+    ACKLAM, ACKLAM_REFINED, AS241, BREAKLESS, BREAKLESS77, qm_abi_version, qm_device_sm_count, qm_moment_row_count,
+    qm_moment_rows, qm_moments, qm_normal_antithetic, qm_normal_philox, qm_normal_quantile, qm_normal_quantile_host,
+    qm_philox_uniform, qm_recycle_exp_to_normal, qm_recycle_normal_to_t, qm_reduce_rows, qm_student_coefficients)

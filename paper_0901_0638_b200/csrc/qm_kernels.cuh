@@ -76,14 +76,17 @@ k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int 
 // ------------------------------------------------- fp32 normal, TMA pipeline
 // pipeline shapes: NC consumer warps (+1 producer), STAGES x TILE floats of
 // shared memory per CTA, MINB CTAs per SM
-template <int NC_, int STAGES_, int TILE_, int MINB_>
+template <int NC_, int STAGES_, int TILE_, int MINB_, int UNROLL_ = 1>
 struct TmaCfg {
     static constexpr int NC = NC_, STAGES = STAGES_, TILE = TILE_, MINB = MINB_, THREADS = 32 * (NC_ + 1);
-    static_assert(TILE_ % (4 * 32 * NC_) == 0, "tile must split evenly over the consumer threads");
+    static constexpr int UNROLL = UNROLL_;
+    static_assert(TILE_ % (4 * 32 * NC_ * UNROLL_) == 0, "tile must split evenly over the consumer threads");
 };
-using TmaCfgA = TmaCfg<16, 4, 8192, 1>;   // 1 CTA/SM, 16 consumer warps, 128 KB
-using TmaCfgB = TmaCfg<16, 3, 8192, 2>;   // 2 CTAs/SM, 32 consumer warps, 2 x 96 KB
-using TmaCfgC = TmaCfg<31, 4, 7936, 1>;   // 1 CTA/SM, 31 consumer warps, 124 KB
+using TmaCfgA = TmaCfg<16, 4, 8192, 1>;      // 1 CTA/SM, 16 consumer warps, 128 KB
+using TmaCfgB = TmaCfg<16, 3, 8192, 2>;      // 2 CTAs/SM, 32 consumer warps, 2 x 96 KB
+using TmaCfgC = TmaCfg<31, 4, 7936, 1>;      // 1 CTA/SM, 31 consumer warps, 124 KB
+using TmaCfgD = TmaCfg<16, 3, 8192, 2, 2>;   // B with two float4 in flight per thread
+using TmaCfgE = TmaCfg<12, 4, 6144, 2>;      // 2 CTAs/SM, 24 consumer warps, 2 x 96 KB
 
 template <int ALG, class CFG>
 struct OpNormalF32 {
@@ -91,7 +94,7 @@ struct OpNormalF32 {
     {
         float4 *t4 = reinterpret_cast<float4 *>(t);
         constexpr int per = CFG::TILE / 4 / (CFG::NC * 32);
-#pragma unroll 1
+#pragma unroll CFG::UNROLL
         for (int j = 0; j < per; ++j) {
             float4 *p = t4 + ctid + j * nct;
             const float4 a = *p;

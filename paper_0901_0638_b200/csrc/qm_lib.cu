@@ -95,7 +95,7 @@ char tma_cfg()
     static char c = 0;
     if (!c) {
         const char *e = getenv("QM_TMA_CFG");
-        c = (e && (e[0] == 'A' || e[0] == 'B' || e[0] == 'C')) ? e[0] : 'B';
+        c = (e && e[0] >= 'A' && e[0] <= 'E') ? e[0] : 'B';
     }
     return c;
 }
@@ -106,6 +106,8 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
     switch (tma_cfg()) {
     case 'A': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
     case 'C': return launch_stream_f32<TmaCfgC>(k_normal_f32_tma<ALG, TmaCfgC>, k_normal_f32<ALG>, u, z, n, s);
+    case 'D': return launch_stream_f32<TmaCfgD>(k_normal_f32_tma<ALG, TmaCfgD>, k_normal_f32<ALG>, u, z, n, s);
+    case 'E': return launch_stream_f32<TmaCfgE>(k_normal_f32_tma<ALG, TmaCfgE>, k_normal_f32<ALG>, u, z, n, s);
     default: return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
     }
 }
@@ -264,11 +266,30 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
     return launched();
 }
 
-qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax, double *sums_dev, void *stream)
+int64_t qm_moment_row_count(int64_t n) { return n > 0 ? moment_rows(n) : 0; }
+
+qm_status qm_moment_rows(const void *x, int64_t n, qm_precision p, double *rows, void *stream)
 {
-    if (n < 0 || (n > 0 && x == nullptr) || sums_dev == nullptr) return QM_EINVAL;
+    if (n < 0 || (n > 0 && (x == nullptr || rows == nullptr)) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    return moment_rows_launch(x, n, p == QM_F64, rows, (cudaStream_t)stream);
+}
+
+qm_status qm_reduce_rows(const double *rows, int64_t nrows, int ncol, double *out, void *stream)
+{
+    if (nrows < 0 || ncol < 1 || ncol > 64 || out == nullptr || (nrows > 0 && rows == nullptr)) return QM_EINVAL;
+    return reduce_rows_launch(rows, nrows, ncol, ncol, out, (cudaStream_t)stream);
+}
+
+qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax, double *sums_dev, double *rows_ws,
+                     void *stream)
+{
+    if (n < 0 || (n > 0 && (x == nullptr || rows_ws == nullptr)) || sums_dev == nullptr) return QM_EINVAL;
     if ((p != QM_F32 && p != QM_F64) || kmax < 1 || kmax > 4) return QM_EINVAL;
-    return moments_launch(x, n, p == QM_F64, kmax, sums_dev, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    qm_status r = (n > 0) ? moment_rows_launch(x, n, p == QM_F64, rows_ws, s) : QM_OK;
+    if (r != QM_OK) return r;
+    return reduce_rows_launch(rows_ws, moment_rows(n), 4, kmax, sums_dev, s);
 }
 
 // ------------------------------------------------------------------ e2e

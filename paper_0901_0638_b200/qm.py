@@ -99,14 +99,40 @@ def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, st
     return z
 
 
-def qm_moments(x: torch.Tensor, kmax: int = 4, workspace=None, stream=None) -> torch.Tensor:
-    """Returns the device workspace; S_k is workspace[k-1] (fp64)."""
+def qm_moment_row_count(n: int) -> int:
+    return L.load().qm_moment_row_count(n)
+
+
+def qm_moment_rows(x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """Fixed-chunk moment rows, shape (qm_moment_row_count(n), 4) fp64."""
     _dev(x, "x")
-    ws = workspace if workspace is not None else torch.empty(L.QM_MOMENTS_WORKSPACE, dtype=torch.float64,
-                                                            device=x.device)
-    L.check("qm_moments", L.load().qm_moments(x.data_ptr(), x.numel(), _prec(x), kmax, ws.data_ptr(),
-                                              _stream(stream)))
-    return ws
+    nr = qm_moment_row_count(x.numel())
+    rows = out if out is not None else torch.empty((nr, 4), dtype=torch.float64, device=x.device)
+    if rows.numel() < 4 * nr or rows.dtype != torch.float64:
+        raise ValueError("rows too small or not float64")
+    L.check("qm_moment_rows", L.load().qm_moment_rows(x.data_ptr(), x.numel(), _prec(x), rows.data_ptr(),
+                                                      _stream(stream)))
+    return rows
+
+
+def qm_reduce_rows(rows: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """Fixed-order column sums of a (nrows, ncol) fp64 matrix."""
+    _dev(rows, "rows")
+    nrows, ncol = rows.shape
+    o = out if out is not None else torch.empty(ncol, dtype=torch.float64, device=rows.device)
+    L.check("qm_reduce_rows", L.load().qm_reduce_rows(rows.data_ptr(), nrows, ncol, o.data_ptr(), _stream(stream)))
+    return o
+
+
+def qm_moments(x: torch.Tensor, kmax: int = 4, out=None, rows=None, stream=None) -> torch.Tensor:
+    """S_k = sum x^k, k = 1..kmax, fp64 on the device (deterministic)."""
+    _dev(x, "x")
+    nr = qm_moment_row_count(x.numel())
+    ws = rows if rows is not None else torch.empty(max(nr, 1) * 4, dtype=torch.float64, device=x.device)
+    o = out if out is not None else torch.empty(kmax, dtype=torch.float64, device=x.device)
+    L.check("qm_moments", L.load().qm_moments(x.data_ptr(), x.numel(), _prec(x), kmax, o.data_ptr(),
+                                              ws.data_ptr(), _stream(stream)))
+    return o
 
 
 def qm_normal_quantile_host(u: torch.Tensor, out=None, alg: int = BREAKLESS) -> torch.Tensor:

@@ -1,0 +1,80 @@
+"""Multi-GPU sharding of the sample stream and the one collective of the path
+(SURVEY §8 row e): samples are independent, so rank r of G maps a contiguous
+slice of the global Philox stream (counter offset = first sample / samples per
+Philox block) and no data crosses GPUs; the only exchange is the all-reduce of
+the moment / Monte-Carlo sums (row a8).
+
+Exactness across G: partial sums live in fixed chunks of the GLOBAL stream
+(``QM_MOMENT_CHUNK`` samples per row, see include/qm.h).  Each rank writes its
+rows into a zeroed global row matrix; all_reduce(SUM) of that matrix is exact
+(one non-zero contributor per row) and the fixed-order ``qm_reduce_rows`` gives
+the same bits for any number of ranks.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+QM_MOMENT_CHUNK = 65536
+WORDS_PER_BLOCK = {4: 4, 8: 2}     # fp32: 4 samples per Philox block, fp64: 2
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    start: int          # first global sample index of this rank
+    count: int          # samples owned by this rank
+    counter_offset: int  # Philox block counter of `start`
+    row0: int           # first global moment row of this rank
+    nrows: int          # moment rows owned by this rank
+
+
+def shard(n_total: int, world: int, rank: int, itemsize: int = 4) -> Shard:
+    """Contiguous shard of a global stream of n_total samples.
+
+    Shard boundaries fall on QM_MOMENT_CHUNK multiples (so every moment row has
+    exactly one owner and Philox blocks never straddle ranks); the last rank
+    takes the remainder."""
+    if world < 1 or not (0 <= rank < world) or n_total < 0:
+        raise ValueError("bad shard arguments")
+    nchunks = -(-n_total // QM_MOMENT_CHUNK)
+    c0 = (nchunks * rank) // world
+    c1 = (nchunks * (rank + 1)) // world
+    start = min(c0 * QM_MOMENT_CHUNK, n_total)
+    end = min(c1 * QM_MOMENT_CHUNK, n_total)
+    wpb = WORDS_PER_BLOCK[itemsize]
+    return Shard(rank, world, start, end - start, start // wpb, c0, c1 - c0)
+
+
+def global_rows(n_total: int) -> int:
+    return -(-n_total // QM_MOMENT_CHUNK)
+
+
+def allreduce_rows(rows, group=None):
+    """all_reduce(SUM) of a zero-padded global row matrix (exact: one non-zero
+    contributor per row).  Works on NCCL (CUDA tensors) and gloo (CPU)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
+    return rows
+
+
+def student_moments(n_total: int, nu: float, K: int, zstar: float, seed: int, rank: int = 0, world: int = 1,
+                    dtype=None, group=None, device=None):
+    """Config 4 on G GPUs: rank r draws its slice of 2^k fp64 standard normals
+    (fused Philox + breakless quantile), recycles them into Student-t (row a6),
+    writes its moment rows, all-reduces the row matrix over NCCL and reduces it
+    in a fixed order.  Returns (sums[4] on the device, local t samples)."""
+    import torch
+
+    from . import qm as Q
+    dtype = dtype or torch.float64
+    itemsize = torch.tensor([], dtype=dtype).element_size()
+    sh = shard(n_total, world, rank, itemsize)
+    z = Q.qm_normal_philox(sh.count, seed, sh.counter_offset, dtype=dtype, device=device)
+    t = Q.qm_recycle_normal_to_t(z, nu, K, zstar)
+    rows = torch.zeros((global_rows(n_total), 4), dtype=torch.float64, device=t.device)
+    if sh.count:
+        Q.qm_moment_rows(t, out=rows[sh.row0:sh.row0 + sh.nrows])
+    allreduce_rows(rows, group)
+    return Q.qm_reduce_rows(rows), t

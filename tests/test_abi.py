@@ -54,7 +54,9 @@ def test_argument_validation_before_launch(lib):
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 5.0, 16, 0.0, None) == L.QM_EINVAL   # zstar needed
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 50.0, 16, 5.0, None) == L.QM_EUNSUPPORTED
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 4.0, 0, 3.9, None) == L.QM_EINVAL
-    assert lib.qm_moments(p, 10, L.QM_F64, 5, p, None) == L.QM_EINVAL
+    assert lib.qm_moments(p, 10, L.QM_F64, 5, p, p, None) == L.QM_EINVAL
+    assert lib.qm_reduce_rows(p, 4, 65, p, None) == L.QM_EINVAL
+    assert lib.qm_moment_row_count(65536 * 3 + 1) == 4
     assert lib.qm_philox_uniform(None, 3, L.QM_F32, 1, 0, None) == L.QM_EINVAL
     assert lib.qm_normal_quantile_host(p, p, -3, L.QM_F32, 0) == L.QM_EINVAL
     assert lib.qm_status_string(L.QM_EUNSUPPORTED).decode() == "unsupported combination"

@@ -51,3 +51,42 @@ def test_moments(dtype):
     assert np.all(np.abs(S - ref) <= 64 * np.finfo(np.float64).eps * absum)
     ws2 = Q.qm_moments(torch.from_numpy(x).cuda(), 4)
     assert torch.equal(ws[:4], ws2[:4])          # deterministic
+
+
+def test_moment_rows_are_device_count_independent():
+    """Config 4 pipeline emulated for G = 1, 2, 4, 8 ranks on one GPU: the row
+    matrix and the fixed-order sums are bit-identical (SURVEY §8 e)."""
+    from paper_0901_0638_b200.shard import global_rows, shard
+    n = 3 * 65536 * 8 + 1000
+    seed = 0x5EEDC0FFEE123457
+    res = []
+    for G in (1, 2, 4, 8):
+        rows = torch.zeros((global_rows(n), 4), dtype=torch.float64, device="cuda")
+        for r in range(G):
+            s = shard(n, G, r, 8)
+            if s.count == 0:
+                continue
+            z = Q.qm_normal_philox(s.count, seed, s.counter_offset, dtype=torch.float64)
+            t = Q.qm_recycle_normal_to_t(z, 5.0, 16, 4.6506)
+            Q.qm_moment_rows(t, out=rows[s.row0:s.row0 + s.nrows])
+        res.append((rows.clone(), Q.qm_reduce_rows(rows)))
+    for rows, sums in res[1:]:
+        assert torch.equal(rows, res[0][0]) and torch.equal(sums, res[0][1])
+
+
+def test_student_moments_vs_oracle_and_theory():
+    """Sums of t^k over the same Philox stream: GPU vs oracle (same formulas), and
+    the sample moments vs E t^2 = nu/(nu-2), E t^4 = 3 nu^2/((nu-2)(nu-4)) (nu = 10)."""
+    from paper_0901_0638_b200.shard import student_moments
+    n, seed, nu = 1 << 20, 1234, 10.0
+    sums, t = student_moments(n, nu, 16, 6.9584, seed)
+    S = sums.cpu().numpy()
+    u = O.philox_uniform(n, seed, 0, np.float64)
+    z = O.normal_breakless(u, O.D13, 64).astype(np.float64)
+    tt = O.student_map(z, nu, 16, 6.9584)
+    ref = O.moments(tt.astype(np.float64), 4).astype(np.float64)
+    absum = np.array([np.sum(np.abs(tt.astype(np.float64)) ** k) for k in range(1, 5)])
+    assert np.all(np.abs(S - ref) <= 1e-13 * absum)
+    m2, m4 = S[1] / n, S[3] / n
+    assert abs(m2 - nu / (nu - 2)) < 6 * np.sqrt((m4 - m2 ** 2) / n)
+    assert abs(m4 / (3 * nu * nu / ((nu - 2) * (nu - 4))) - 1) < 0.1
