@@ -227,6 +227,12 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     zo = torch.empty_like(v)
     rec("exp_to_normal_f32_2^28", lambda: Q.qm_recycle_exp_to_normal(v, out=zo), n, 8)
     del v, zo
+    # config 5: 2^34-sample exponential-base Monte-Carlo call sweep, 17 strikes (Philox-fused)
+    strikes = list(np.linspace(50, 150, 17))
+    rows = torch.empty((Q.qm_mc_row_count(1 << 34), 34), dtype=torch.float64, device="cuda")
+    rec("mc_call_sweep_f32_2^34_17K",
+        lambda: Q.qm_mc_european_call(1 << 34, SEED, 0, 100.0, 0.05, 0.2, 1.0, strikes, out=rows), 1 << 34, 0)
+    del rows
     # config 1: 2^20 fp64, breakless vs branching baselines (tail-stratified input)
     u1 = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
     z1 = torch.empty_like(u1)

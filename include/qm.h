@@ -129,6 +129,28 @@ qm_status qm_reduce_rows(const double *rows, int64_t nrows, int ncol, double *ou
 qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax,
                      double *sums_dev, double *rows_ws, void *stream);
 
+/* Monte-Carlo European-call sweep (BASELINE.json config 5) with normal
+ * innovations from the EXPONENTIAL base: sample i of
+ * the Philox stream (fp32 grid, qm_philox_uniform layout) gives v = -log u,
+ * a sign from bit 8 of the Philox word, Z = sign * Q(v) (App C rational), and
+ * S_T = S0 exp((r - sigma^2/2) T + sigma sqrt(T) Z).  For each of the
+ * nstrikes <= 32 strikes K_j, row r (fixed chunk r of QM_MC_CHUNK samples)
+ * receives rows[r*2*nstrikes + 2j] = sum (S_T - K_j)^+ and [.. + 2j+1] = sum of
+ * its square.  rows: qm_mc_row_count(n) * 2 * nstrikes doubles (device).
+ * Rows are all-reduced across GPUs exactly and added by qm_reduce_rows; the
+ * price is exp(-rT) * sum / n.  Accumulation: fp32 over 64 samples per
+ * thread, then fp64. */
+#define QM_MC_CHUNK (1 << 20)
+#define QM_MC_MAX_STRIKES 32
+typedef struct {
+    double S0, r, sigma, T;
+    int nstrikes;
+    double strikes[QM_MC_MAX_STRIKES];
+} qm_mc_params;
+int64_t   qm_mc_row_count(int64_t n);
+qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset, const qm_mc_params *params,
+                              double *rows, void *stream);
+
 /* End-to-end variant of qm_normal_quantile on HOST buffers: copies u in,
  * computes, copies z out, overlapping the three in chunks on library-owned
  * streams and pinned/device staging buffers (allocated once per thread and

@@ -27,7 +27,7 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 _SO = _HERE / "liboracle.so"
-_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c"]
+_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_mc.c"]
 
 # formula ids of the oracle (local to the oracle; the product has its own enum)
 C55, A77, D13 = 55, 77, 13
@@ -84,6 +84,7 @@ def lib():
             "orc_student_cdf_upper_v": (None, [P, P, i64, dbl]),
             "orc_moments_f64": (None, [P, i64, i32, P]),
             "orc_moments_f32": (None, [P, i64, i32, P]),
+            "orc_mc_call": (None, [i64, u64, u64, dbl, dbl, dbl, dbl, P, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -310,3 +311,23 @@ def moments(x, kmax: int = 4) -> np.ndarray:
         x = _in(x)
         lib().orc_moments_f64(_p(x), x.size, kmax, _p(S))
     return S
+
+
+# -------------------------------------------------------- Monte Carlo (config 5)
+def mc_call(n: int, seed: int, counter_offset: int, S0: float, r: float, sigma: float, T: float, strikes):
+    """Sums of (S_T - K)^+ and its square per strike over n exponential-base samples (orc_mc.c)."""
+    K = _in(strikes)
+    out = np.zeros(2 * K.size, np.longdouble)
+    lib().orc_mc_call(n, seed, counter_offset, S0, r, sigma, T, _p(K), K.size, _p(out))
+    return out.reshape(-1, 2)
+
+
+def black_scholes_call(S0: float, K, r: float, sigma: float, T: float) -> np.ndarray:
+    """Closed-form European call (the pin of the Monte-Carlo sweep), via mpmath."""
+    import mpmath as mp
+    out = []
+    for k in np.atleast_1d(K):
+        d1 = (mp.log(S0 / k) + (r + sigma * sigma / 2) * T) / (sigma * mp.sqrt(T))
+        d2 = d1 - sigma * mp.sqrt(T)
+        out.append(float(S0 * mp.ncdf(d1) - k * mp.exp(-r * T) * mp.ncdf(d2)))
+    return np.array(out)

@@ -426,3 +426,12 @@ int orc_normal_acklam(const double *u, ld *out, int64_t n, int prec, int refine)
     for (int64_t i = 0; i < n; ++i) out[i] = acklam_one((ld)u[i], prec, refine);
     return 0;
 }
+
+/* Q(v) of App C with float-rounded coefficients (for orc_mc.c) */
+ld orc_Q_C55_f32coef(ld v)
+{
+    static rat_t r;
+    static int init = 0;
+    if (!init) { get_rat(ORC_C55, 32, &r); init = 1; }
+    return rational_Q(&r, v);
+}

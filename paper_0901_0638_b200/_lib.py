@@ -15,6 +15,15 @@ QM_OK, QM_EINVAL, QM_EUNSUPPORTED, QM_ECUDA = 0, 1, 2, 3
 QM_F32, QM_F64 = 1, 2
 QM_BREAKLESS, QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED = 0, 1, 2, 3, 4
 QM_MOMENT_CHUNK = 65536
+QM_MC_CHUNK = 1 << 20
+QM_MC_MAX_STRIKES = 32
+
+
+class McParams(ctypes.Structure):
+    """qm_mc_params of include/qm.h"""
+    _fields_ = [("S0", ctypes.c_double), ("r", ctypes.c_double), ("sigma", ctypes.c_double),
+                ("T", ctypes.c_double), ("nstrikes", ctypes.c_int),
+                ("strikes", ctypes.c_double * QM_MC_MAX_STRIKES)]
 
 # every symbol include/qm.h declares, with (restype, argtypes)
 _P, _I64, _I32, _U64, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_double
@@ -28,6 +37,8 @@ SIGNATURES = {
     "qm_normal_philox": (_I32, [_P, _I64, _I32, _I32, _U64, _U64, _P]),
     "qm_recycle_normal_to_t": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P]),
     "qm_recycle_exp_to_normal": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
+    "qm_mc_row_count": (_I64, [_I64]),
+    "qm_mc_european_call": (_I32, [_I64, _U64, _U64, _P, _P, _P]),
     "qm_moment_row_count": (_I64, [_I64]),
     "qm_moment_rows": (_I32, [_P, _I64, _I32, _P, _P]),
     "qm_reduce_rows": (_I32, [_P, _I64, _I32, _P, _P]),

@@ -14,6 +14,8 @@
 #include "qm_baselines.cuh"
 #include "qm_student.cuh"
 #include "qm_moments.cuh"
+#include "qm_mc.cuh"
+#include <cmath>
 
 using namespace qm;
 
@@ -264,6 +266,35 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
     if (p == QM_F64) k_student_f64<<<g, kThreads, 0, s>>>((const double *)z, (double *)t, n, sp);
     else k_student_f32<<<g, kThreads, 0, s>>>((const float *)z, (float *)t, n, sp);
     return launched();
+}
+
+int64_t qm_mc_row_count(int64_t n) { return n > 0 ? (n + QM_MC_CHUNK - 1) / QM_MC_CHUNK : 0; }
+
+qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset, const qm_mc_params *params,
+                              double *rows, void *stream)
+{
+    if (n < 0 || params == nullptr || (n > 0 && rows == nullptr)) return QM_EINVAL;
+    const int nk = params->nstrikes;
+    if (nk < 1 || nk > QM_MC_MAXK || !(params->S0 > 0.0) || !(params->sigma >= 0.0) || !(params->T >= 0.0))
+        return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    McParams mp;
+    mp.a = (float)(log(params->S0) + (params->r - 0.5 * params->sigma * params->sigma) * params->T);
+    mp.b = (float)(params->sigma * sqrt(params->T));
+    mp.nk = nk;
+    for (int j = 0; j < QM_MC_MAXK; ++j) mp.K[j] = (j < nk) ? (float)params->strikes[j] : 0.0f;
+    const size_t smem = (size_t)2 * nk * 256 * sizeof(double);
+    const int64_t nrows = qm_mc_row_count(n);
+    cudaStream_t s = (cudaStream_t)stream;
+    auto go = [&](auto kern) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return QM_ECUDA;
+        kern<<<(unsigned)nrows, 256, smem, s>>>(n, seed, counter_offset, mp, rows);
+        return launched();
+    };
+    if (nk <= 8) return go(k_mc_call<8>);
+    if (nk <= 17) return go(k_mc_call<17>);
+    return go(k_mc_call<32>);
 }
 
 int64_t qm_moment_row_count(int64_t n) { return n > 0 ? moment_rows(n) : 0; }

@@ -1,0 +1,96 @@
+// qm_mc.cuh -- config 5: Philox-fused Monte-Carlo European-call sweep whose
+// normal innovations come from the EXPONENTIAL base.
+//
+// Per sample (the oracle's orc_mc.c states the same recipe):
+//   w = Philox word (stream layout of qm_philox_uniform, fp32 grid)
+//   v = -log u, u = (2 (w >> 9) + 1) 2^-24       one-sided unit exponential
+//   s = +1 if bit 8 of w is set, else -1          two-sided (Laplace) base
+//   Z = s Q(v)                                    App C rational, no reflection needed
+//   S_T = exp(a + b Z), a = log S0 + (r - sigma^2/2) T, b = sigma sqrt(T)
+//   per strike j: (S_T - K_j)^+ and its square.
+// Sums: fp32 partials over 64 samples per thread, flushed into fp64
+// accumulators in shared memory; one CTA per fixed chunk of QM_MC_CHUNK samples
+// of the GLOBAL stream writes one row [sum p_0, sum p_0^2, sum p_1, ...]; rows
+// are all-reduced exactly across GPUs and added by qm_reduce_rows (fixed order).
+#pragma once
+#include "qm_math.cuh"
+
+#define QM_MC_CHUNK (1 << 20)
+#define QM_MC_MAXK 32
+
+namespace qm {
+
+struct McParams {
+    float a, b;                 // log-price drift and volatility scale
+    int nk;                     // number of strikes (<= QM_MC_MAXK)
+    float K[QM_MC_MAXK];
+};
+
+// NKMAX: register budget for the per-thread fp32 partials (instantiated for 8, 17, 32)
+template <int NKMAX>
+__global__ void __launch_bounds__(256)
+k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __grid_constant__ McParams mp,
+          double *__restrict__ rows)
+{
+    extern __shared__ double acc[];            // [2 * nk][256]
+    const int nk = mp.nk, tid = threadIdx.x;
+    for (int j = 0; j < 2 * nk; ++j) acc[j * 256 + tid] = 0.0;
+
+    const int64_t s0 = (int64_t)blockIdx.x * QM_MC_CHUNK;
+    const int64_t s1 = (s0 + QM_MC_CHUNK < n) ? s0 + QM_MC_CHUNK : n;
+    const int64_t b0 = s0 >> 2, b1 = (s1 + 3) >> 2;         // Philox blocks of this chunk
+    float part[2 * NKMAX];
+    int inpart = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * NKMAX; ++j) part[j] = 0.0f;
+
+    for (int64_t blk = b0 + tid; blk < b1; blk += 256) {
+        const uint4 w = philox_block(c0 + (unsigned long long)blk, seed);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        float u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) u[k] = u01_f32(ws[k]);
+        const float2 v01 = neg_log2x_f32x2(u[0], u[1], -1);      // -log u
+        const float2 v23 = neg_log2x_f32x2(u[2], u[3], -1);
+        const float v[4] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = 4 * blk + k;
+            float z = rat32<ALG_BREAKLESS>(v[k]);
+            z = ((ws[k] >> 8) & 1u) ? z : -z;
+            const float ST = expf(__fmaf_rn(mp.b, z, mp.a));
+            const bool in = i < s1;
+#pragma unroll
+            for (int j = 0; j < NKMAX; ++j) {
+                if (j < nk) {
+                    const float p = in ? fmaxf(__fsub_rn(ST, mp.K[j]), 0.0f) : 0.0f;
+                    part[2 * j] = __fadd_rn(part[2 * j], p);
+                    part[2 * j + 1] = __fmaf_rn(p, p, part[2 * j + 1]);
+                }
+            }
+        }
+        if (++inpart == 16) {                   // 64 samples: flush into fp64
+            inpart = 0;
+#pragma unroll
+            for (int j = 0; j < 2 * NKMAX; ++j) {
+                if (j < 2 * nk) {
+                    acc[j * 256 + tid] = __dadd_rn(acc[j * 256 + tid], (double)part[j]);
+                    part[j] = 0.0f;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * NKMAX; ++j)
+        if (j < 2 * nk) acc[j * 256 + tid] = __dadd_rn(acc[j * 256 + tid], (double)part[j]);
+    __syncthreads();
+    // fixed tree over the 256 threads, column by column
+    for (int w = 128; w > 0; w >>= 1) {
+        if (tid < w)
+            for (int j = 0; j < 2 * nk; ++j) acc[j * 256 + tid] = __dadd_rn(acc[j * 256 + tid], acc[j * 256 + tid + w]);
+        __syncthreads();
+    }
+    if (tid < 2 * nk) rows[(int64_t)blockIdx.x * 2 * nk + tid] = acc[tid * 256];
+}
+
+}  // namespace qm

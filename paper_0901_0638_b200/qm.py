@@ -99,6 +99,28 @@ def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, st
     return z
 
 
+def qm_mc_row_count(n: int) -> int:
+    return L.load().qm_mc_row_count(n)
+
+
+def qm_mc_european_call(n: int, seed: int, counter_offset: int, S0: float, r: float, sigma: float, T: float,
+                        strikes, out=None, device=None, stream=None) -> torch.Tensor:
+    """Config-5 Monte-Carlo call sweep rows, shape (qm_mc_row_count(n), 2 * nstrikes) fp64."""
+    import ctypes
+    ks = [float(k) for k in strikes]
+    if not 1 <= len(ks) <= L.QM_MC_MAX_STRIKES:
+        raise ValueError("1..32 strikes")
+    p = L.McParams(S0, r, sigma, T, len(ks), (ctypes.c_double * L.QM_MC_MAX_STRIKES)(*ks))
+    nr = qm_mc_row_count(n)
+    rows = out if out is not None else torch.empty((max(nr, 1), 2 * len(ks)), dtype=torch.float64,
+                                                   device=device or "cuda")
+    if rows.numel() < nr * 2 * len(ks):
+        raise ValueError("rows too small")
+    L.check("qm_mc_european_call", L.load().qm_mc_european_call(n, seed, counter_offset, ctypes.byref(p),
+                                                                rows.data_ptr(), _stream(stream)))
+    return rows
+
+
 def qm_moment_row_count(n: int) -> int:
     return L.load().qm_moment_row_count(n)
 

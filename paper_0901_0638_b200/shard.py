@@ -15,6 +15,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 QM_MOMENT_CHUNK = 65536
+QM_MC_CHUNK = 1 << 20
 WORDS_PER_BLOCK = {4: 4, 8: 2}     # fp32: 4 samples per Philox block, fp64: 2
 
 
@@ -29,19 +30,19 @@ class Shard:
     nrows: int          # moment rows owned by this rank
 
 
-def shard(n_total: int, world: int, rank: int, itemsize: int = 4) -> Shard:
+def shard(n_total: int, world: int, rank: int, itemsize: int = 4, chunk: int = QM_MOMENT_CHUNK) -> Shard:
     """Contiguous shard of a global stream of n_total samples.
 
-    Shard boundaries fall on QM_MOMENT_CHUNK multiples (so every moment row has
-    exactly one owner and Philox blocks never straddle ranks); the last rank
-    takes the remainder."""
+    Shard boundaries fall on `chunk` multiples (QM_MOMENT_CHUNK for moment rows,
+    QM_MC_CHUNK for Monte-Carlo rows), so every row has exactly one owner and
+    Philox blocks never straddle ranks; the last rank takes the remainder."""
     if world < 1 or not (0 <= rank < world) or n_total < 0:
         raise ValueError("bad shard arguments")
-    nchunks = -(-n_total // QM_MOMENT_CHUNK)
+    nchunks = -(-n_total // chunk)
     c0 = (nchunks * rank) // world
     c1 = (nchunks * (rank + 1)) // world
-    start = min(c0 * QM_MOMENT_CHUNK, n_total)
-    end = min(c1 * QM_MOMENT_CHUNK, n_total)
+    start = min(c0 * chunk, n_total)
+    end = min(c1 * chunk, n_total)
     wpb = WORDS_PER_BLOCK[itemsize]
     return Shard(rank, world, start, end - start, start // wpb, c0, c1 - c0)
 
@@ -78,3 +79,28 @@ def student_moments(n_total: int, nu: float, K: int, zstar: float, seed: int, ra
         Q.qm_moment_rows(t, out=rows[sh.row0:sh.row0 + sh.nrows])
     allreduce_rows(rows, group)
     return Q.qm_reduce_rows(rows), t
+
+
+def mc_call_sweep(n_total: int, seed: int, S0: float, r: float, sigma: float, T: float, strikes,
+                  rank: int = 0, world: int = 1, group=None, device=None):
+    """Config 5 on G GPUs: rank r prices its slice of the exponential-base
+    Monte-Carlo stream (qm_mc_european_call), writes its rows into a zeroed
+    global row matrix, all-reduces it over NCCL and reduces it in a fixed order.
+    Returns (prices[nstrikes], standard errors[nstrikes]) as CUDA tensors."""
+    import math
+
+    import torch
+
+    from . import qm as Q
+    ks = list(strikes)
+    sh = shard(n_total, world, rank, 4, QM_MC_CHUNK)
+    rows = torch.zeros((-(-n_total // QM_MC_CHUNK), 2 * len(ks)), dtype=torch.float64, device=device or "cuda")
+    if sh.count:
+        Q.qm_mc_european_call(sh.count, seed, sh.counter_offset, S0, r, sigma, T, ks,
+                              out=rows[sh.row0:sh.row0 + sh.nrows])
+    allreduce_rows(rows, group)
+    sums = Q.qm_reduce_rows(rows).view(-1, 2)
+    disc = math.exp(-r * T)
+    mean = sums[:, 0] / n_total
+    var = sums[:, 1] / n_total - mean * mean
+    return disc * mean, disc * torch.sqrt(var.clamp_min(0) / n_total)

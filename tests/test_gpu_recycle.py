@@ -90,3 +90,40 @@ def test_student_moments_vs_oracle_and_theory():
     m2, m4 = S[1] / n, S[3] / n
     assert abs(m2 - nu / (nu - 2)) < 6 * np.sqrt((m4 - m2 ** 2) / n)
     assert abs(m4 / (3 * nu * nu / ((nu - 2) * (nu - 4))) - 1) < 0.1
+
+
+# ------------------------------------------------ config 5: Monte-Carlo sweep
+STRIKES = list(np.linspace(50, 150, 17))
+
+
+def test_mc_rows_vs_oracle():
+    """Same Philox stream, same exponential-base recipe: GPU sums vs the oracle's
+    long-double sums (fp32 per-sample arithmetic, fp32->fp64 partials: 2e-5 relative)."""
+    n, seed, c0 = (1 << 18) + 1000, 99, 12
+    rows = Q.qm_mc_european_call(n, seed, c0, 100.0, 0.05, 0.2, 1.0, STRIKES)
+    got = Q.qm_reduce_rows(rows).view(-1, 2).cpu().numpy()
+    ref = O.mc_call(n, seed, c0, 100.0, 0.05, 0.2, 1.0, STRIKES).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 2e-5 * np.abs(ref) + 1e-3)
+
+
+def test_mc_price_vs_black_scholes_and_device_count():
+    """2^26 samples: every strike within 4 standard errors of Black-Scholes; the
+    sweep gives the same bits when sharded over G = 1, 2, 4 ranks (emulated)."""
+    from paper_0901_0638_b200.shard import mc_call_sweep
+    n = 1 << 26
+    price, se = mc_call_sweep(n, 2024, 100.0, 0.05, 0.2, 1.0, STRIKES)
+    bs = O.black_scholes_call(100.0, STRIKES, 0.05, 0.2, 1.0)
+    z = np.abs(price.cpu().numpy() - bs) / se.cpu().numpy()
+    assert z.max() < 4.0, z
+    import torch.nn.functional  # noqa: F401
+    from paper_0901_0638_b200.shard import QM_MC_CHUNK, shard
+    ref_rows = None
+    for G in (1, 2, 4):
+        rows = torch.zeros((n // QM_MC_CHUNK, 2 * len(STRIKES)), dtype=torch.float64, device="cuda")
+        for r in range(G):
+            s = shard(n, G, r, 4, QM_MC_CHUNK)
+            Q.qm_mc_european_call(s.count, 2024, s.counter_offset, 100.0, 0.05, 0.2, 1.0, STRIKES,
+                                  out=rows[s.row0:s.row0 + s.nrows])
+        if ref_rows is None:
+            ref_rows = rows
+        assert torch.equal(rows, ref_rows)
