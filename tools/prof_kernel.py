@@ -32,6 +32,21 @@ elif name.startswith("config1_"):
     u = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
     z = torch.empty_like(u)
     fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
+elif name == "exp2n_f32":
+    import numpy as np
+    from synth import inputs as I
+    v = torch.from_numpy(I.laplace(n, dtype=np.float32)).cuda()
+    z = torch.empty_like(v)
+    fn = lambda: Q.qm_recycle_exp_to_normal(v, out=z)
+elif name == "moments":
+    x = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
+    rows = torch.empty(4 * Q.qm_moment_row_count(1 << 30), dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_moments(x, 4, rows=rows)
+elif name == "mc":
+    import numpy as np
+    ks = list(np.linspace(50, 150, 17))
+    rows = torch.empty((Q.qm_mc_row_count(1 << 32), 34), dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_mc_european_call(1 << 32, SEED, 0, 100.0, 0.05, 0.2, 1.0, ks, out=rows)
 elif name == "student":
     zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
     t = torch.empty_like(zn)
