@@ -99,8 +99,12 @@ QM_DEV dd dd_exp(dd x)
         const dd c = (i == 3) ? dd{1.0 / 6, 9.25185853854297e-18} : (i == 5) ? dd{1.0 / 120, 1.1564823173178713963e-19} : (i == 4) ? dd{1.0 / 24, 2.3129646346357427925e-18} : dd{inv_fact[i], 0.0};
         s = dd_add(s, c);
     }
-    const double sc = scalbn(1.0, (int)k);
-    return dd{s.hi * sc, s.lo * sc};
+    // 2^k as two exact powers of two built from exponent bits (no branches;
+    // |k| <= 2044 keeps both halves in the normal range)
+    const int ki = (int)k, k1 = ki / 2, k2 = ki - k1;
+    const double sc1 = __longlong_as_double((long long)(k1 + 1023) << 52);
+    const double sc2 = __longlong_as_double((long long)(k2 + 1023) << 52);
+    return dd{s.hi * sc1 * sc2, s.lo * sc1 * sc2};
 }
 
 // -log(x) as dd for any positive finite x (subnormals pre-scaled by 2^54)

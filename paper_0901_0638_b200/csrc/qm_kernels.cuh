@@ -120,6 +120,66 @@ struct OpNormalF32 {
     }
 };
 
+// Software-pipelined variant: the fp32 log of float4 j+1 is computed in the
+// same iteration as the FP64 rational of float4 j, so the FP32/ALU work of one
+// sample overlaps the FP64 chain of the previous one inside each thread.
+template <int ALG, class CFG>
+struct OpNormalF32Pipe {
+    QM_DEV static void logs(const float4 a, float4 &zl, float4 &om)
+    {
+        om = make_float4(__fsub_rn(1.0f, a.x), __fsub_rn(1.0f, a.y), __fsub_rn(1.0f, a.z), __fsub_rn(1.0f, a.w));
+        const float2 l01 = neg_log2x_f32x2(fminf(a.x, om.x), fminf(a.y, om.y));
+        const float2 l23 = neg_log2x_f32x2(fminf(a.z, om.z), fminf(a.w, om.w));
+        zl = make_float4(l01.x, l01.y, l23.x, l23.y);
+    }
+    QM_DEV static bool normal(const float4 a)
+    {
+        return (fminf(a.x, __fsub_rn(1.0f, a.x)) >= 1.17549435e-38f) & (fminf(a.y, __fsub_rn(1.0f, a.y)) >= 1.17549435e-38f) &
+               (fminf(a.z, __fsub_rn(1.0f, a.z)) >= 1.17549435e-38f) & (fminf(a.w, __fsub_rn(1.0f, a.w)) >= 1.17549435e-38f);
+    }
+    QM_DEV void tile(float *t, int ctid, int nct) const
+    {
+        float4 *t4 = reinterpret_cast<float4 *>(t);
+        constexpr int per = CFG::TILE / 4 / (CFG::NC * 32);
+        // a whole tile is normal for every grid input; otherwise take the careful path
+        bool ok = true;
+#pragma unroll 4
+        for (int j = 0; j < per; ++j) ok &= normal(t4[ctid + j * nct]);
+        if (!__all_sync(0xffffffffu, ok)) {
+#pragma unroll 1
+            for (int j = 0; j < per; ++j) {
+                float4 *p = t4 + ctid + j * nct;
+                const float4 a = *p;
+                *p = make_float4(nq_f32_careful<ALG>(a.x), nq_f32_careful<ALG>(a.y), nq_f32_careful<ALG>(a.z),
+                                 nq_f32_careful<ALG>(a.w));
+            }
+            return;
+        }
+        float4 a = t4[ctid], zl, om;
+        logs(a, zl, om);
+#pragma unroll 1
+        for (int j = 0; j < per; ++j) {
+            float4 an = a, zn = zl, omn = om;
+            if (j + 1 < per) {
+                an = t4[ctid + (j + 1) * nct];
+                logs(an, zn, omn);
+            }
+            t4[ctid + j * nct] = make_float4(apply_sign_f32(rat32<ALG>(zl.x), a.x, om.x),
+                                             apply_sign_f32(rat32<ALG>(zl.y), a.y, om.y),
+                                             apply_sign_f32(rat32<ALG>(zl.z), a.z, om.z),
+                                             apply_sign_f32(rat32<ALG>(zl.w), a.w, om.w));
+            a = an; zl = zn; om = omn;
+        }
+    }
+};
+
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
+k_normal_f32_tma_pipe(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
+{
+    tma_stream_map<float, CFG::TILE, CFG::STAGES, CFG::NC>(u, z, ntiles, OpNormalF32Pipe<ALG, CFG>{});
+}
+
 template <int ALG, class CFG>
 __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
 k_normal_f32_tma(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
@@ -129,10 +189,11 @@ k_normal_f32_tma(const float *__restrict__ u, float *__restrict__ z, int64_t nti
 
 // ------------------------------------------------------------ fp64 normal
 template <int ALG>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, int vec)
 {
-    constexpr int V = 2;                                  // double2 per lane per chunk
+    constexpr int V = 1;                                  // double2 per lane per chunk (FP64-bound:
+                                                          // occupancy over ILP)
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;

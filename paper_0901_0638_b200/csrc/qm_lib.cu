@@ -97,7 +97,7 @@ char tma_cfg()
     static char c = 0;
     if (!c) {
         const char *e = getenv("QM_TMA_CFG");
-        c = (e && e[0] >= 'A' && e[0] <= 'E') ? e[0] : 'B';
+        c = (e && e[0] >= 'A' && e[0] <= 'G') ? e[0] : 'B';
     }
     return c;
 }
@@ -110,6 +110,8 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
     case 'C': return launch_stream_f32<TmaCfgC>(k_normal_f32_tma<ALG, TmaCfgC>, k_normal_f32<ALG>, u, z, n, s);
     case 'D': return launch_stream_f32<TmaCfgD>(k_normal_f32_tma<ALG, TmaCfgD>, k_normal_f32<ALG>, u, z, n, s);
     case 'E': return launch_stream_f32<TmaCfgE>(k_normal_f32_tma<ALG, TmaCfgE>, k_normal_f32<ALG>, u, z, n, s);
+    case 'F': return launch_stream_f32<TmaCfgB>(k_normal_f32_tma_pipe<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
+    case 'G': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma_pipe<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
     default: return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
     }
 }

@@ -25,7 +25,9 @@ QM_DEV double student_central(const StudentParams &sp, double a)
     const double yh = __dmul_rn(a, a);
     const double yl = __fma_rn(a, a, -yh);
     double s = sp.c[sp.K], c = 0.0;
-    for (int i = sp.K - 1; i >= 0; --i) {
+    int i = sp.K - 1;
+    for (; i >= sp.kc; --i) s = __fma_rn(s, yh, sp.c[i]);      // high-order steps: plain
+    for (; i >= 0; --i) {                                      // last kc steps: compensated
         const double p = __dmul_rn(s, yh);
         const double pi = __fma_rn(s, yh, -p);
         const double t = __dadd_rn(p, sp.c[i]);
@@ -59,7 +61,8 @@ QM_DEV double student_map(const StudentParams &sp, double z, bool any_tail)
     const double a = fabs(z);
     double t = student_central(sp, a);
     if (any_tail) {
-        const double tt = student_tail(sp, fmax(a, 1.0));
+        // every lane of the warp evaluates the tail at a >= z* (one erfcx region)
+        const double tt = student_tail(sp, fmax(a, sp.zstar));
         t = (a >= sp.zstar) ? tt : t;
     }
     t = (a == __longlong_as_double(0x7ff0000000000000LL)) ? a : t;

@@ -9,6 +9,7 @@ namespace qm {
 struct StudentParams {
     double c[QM_STUDENT_KMAX + 1];   // c_0..c_K of the central series
     int K;
+    int kc;                          // number of compensated (error-free) final Horner steps
     double zstar;                    // crossover
     // double-double constants: in the far tail log w ~ -700, so 1/nu must carry
     // more than 53 bits for w^(-1/nu) to stay within an ulp
