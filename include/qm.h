@@ -50,9 +50,16 @@ typedef enum { QM_F32 = 1, QM_F64 = 2 } qm_precision;
  *                  (13,13) in fp64.
  *  QM_BREAKLESS77  the (7,7) rational of App A/B.
  *  QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED  the branching comparison quantiles of
- *                  the paper's Table 3; fp64 only. */
+ *                  the paper's Table 3; fp64 only.
+ *  QM_BREAKLESS_TAIL  QM_BREAKLESS below v = vc and the supplementary tail model
+ *                  Q = sqrt(2 q(a,b)) of §5.1 above: vc = 37 (fp32,
+ *                  App C) or 86.75 (fp64, App D).  Keeps the precision in
+ *                  the deep tail (u < 4.3e-17 in fp32, u < 1e-38 in fp64) at no
+ *                  cost elsewhere (warp-uniform switch).  Normal quantile,
+ *                  antithetic and exponential-base entry points. */
 typedef enum {
-    QM_BREAKLESS = 0, QM_BREAKLESS77 = 1, QM_AS241 = 2, QM_ACKLAM = 3, QM_ACKLAM_REFINED = 4
+    QM_BREAKLESS = 0, QM_BREAKLESS77 = 1, QM_AS241 = 2, QM_ACKLAM = 3, QM_ACKLAM_REFINED = 4,
+    QM_BREAKLESS_TAIL = 5
 } qm_algorithm;
 
 int         qm_abi_version(void);

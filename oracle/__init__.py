@@ -27,7 +27,7 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 _SO = _HERE / "liboracle.so"
-_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_mc.c"]
+_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_mc.c", "orc_tail.c"]
 
 # formula ids of the oracle (local to the oracle; the product has its own enum)
 C55, A77, D13 = 55, 77, 13
@@ -85,6 +85,8 @@ def lib():
             "orc_moments_f64": (None, [P, i64, i32, P]),
             "orc_moments_f32": (None, [P, i64, i32, P]),
             "orc_mc_call": (None, [i64, u64, u64, dbl, dbl, dbl, dbl, P, i32, P]),
+            "orc_normal_breakless_tail": (i32, [P, P, i64, i32, i32, dbl]),
+            "orc_exp_to_normal_tail": (i32, [P, P, i64, i32, i32, dbl]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -183,6 +185,19 @@ def normal_antithetic(u, formula: int, prec: int) -> np.ndarray:
 def exp_to_normal(v, formula: int, prec: int) -> np.ndarray:
     v = _in(v); o = np.empty(v.shape, np.longdouble)
     _chk(lib().orc_exp_to_normal(_p(v), _p(o), v.size, formula, prec))
+    return o
+
+
+def normal_breakless_tail(u, formula: int, prec: int, vc: float) -> np.ndarray:
+    """Composite of row f2: rational for v < vc, the §5.1 tail model beyond (orc_tail.c)."""
+    u = _in(u); o = np.empty(u.shape, np.longdouble)
+    _chk(lib().orc_normal_breakless_tail(_p(u), _p(o), u.size, formula, prec, vc))
+    return o
+
+
+def exp_to_normal_tail(v, formula: int, prec: int, vc: float) -> np.ndarray:
+    v = _in(v); o = np.empty(v.shape, np.longdouble)
+    _chk(lib().orc_exp_to_normal_tail(_p(v), _p(o), v.size, formula, prec, vc))
     return o
 
 

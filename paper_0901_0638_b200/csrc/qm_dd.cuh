@@ -121,6 +121,31 @@ QM_DEV dd dd_log(double x)
     return dd{-m.hi, -m.lo};
 }
 
+// §5.1 supplementary tail model (reading R1): Q(v) = sqrt(2 q(a,b)),
+// a = v - 1/2 log pi, b = log a,
+// q = a - b/2 + (b/4 - 1/2)/a + (b^2 - 6b + 14)/(16 a^2) + (2b^3 - 21b^2 + 102b - 214)/(96 a^3)
+//       + (3b^4 - 46b^3 + 348b^2 - 1488b + 2978)/(384 a^4).
+// a - b/2 in double-double, the small corrections in double, dd sqrt.
+QM_DEV double tail_model_q_dd(dd v)
+{
+    const double C_HI = 0.5723649429247001, C_LO = 5.1329755813539131214e-18;   // log(pi)/2
+    dd a = two_sum(v.hi, -C_HI);
+    a = dd_norm(a.hi, __dadd_rn(a.lo, __dadd_rn(v.lo, -C_LO)));
+    dd b = dd_log(a.hi);
+    b = dd_add_d(b, a.lo / a.hi);                                   // log(a_hi + a_lo)
+    const double bh = b.hi, ia = 1.0 / a.hi;
+    const double t1 = (0.25 * bh - 0.5) * ia;
+    const double t2 = ((bh - 6.0) * bh + 14.0) * (1.0 / 16.0) * ia * ia;
+    const double t3 = (((2.0 * bh - 21.0) * bh + 102.0) * bh - 214.0) * (1.0 / 96.0) * ia * ia * ia;
+    const double t4 = ((((3.0 * bh - 46.0) * bh + 348.0) * bh - 1488.0) * bh + 2978.0) * (1.0 / 384.0) * ia * ia * ia * ia;
+    dd q = dd_add(a, dd{-0.5 * b.hi, -0.5 * b.lo});
+    q = dd_add_d(q, t1 + t2 + t3 + t4);
+    const dd s = dd_sqrt(dd{2.0 * q.hi, 2.0 * q.lo});
+    return s.hi + s.lo;
+}
+
+QM_DEV double tail_model_q(double v) { return tail_model_q_dd(dd{v, 0.0}); }
+
 // Compensated Horner for arbitrary-sign coefficients at a dd point, fully compensated.
 template <int N>
 QM_DEV dd horner_dd(const double *a, dd z)

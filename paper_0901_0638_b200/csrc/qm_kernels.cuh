@@ -45,15 +45,15 @@ k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int 
         }
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 4 * V; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= 1.17549435e-38f);
+        for (int k = 0; k < 4 * V; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= fast_vv_min_f32<ALG>());
         float y[4 * V];
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
             for (int k = 0; k < 4 * V; k += 2) {
                 const float oa = __fsub_rn(1.0f, x[k]), ob = __fsub_rn(1.0f, x[k + 1]);
                 const float2 lz = neg_log2x_f32x2(fminf(x[k], oa), fminf(x[k + 1], ob));
-                y[k] = apply_sign_f32(rat32<ALG>(lz.x), x[k], oa);
-                y[k + 1] = apply_sign_f32(rat32<ALG>(lz.y), x[k + 1], ob);
+                y[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.x), x[k], oa);
+                y[k + 1] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.y), x[k + 1], ob);
             }
         } else {
 #pragma unroll
@@ -87,6 +87,8 @@ using TmaCfgB = TmaCfg<16, 3, 8192, 2>;      // 2 CTAs/SM, 32 consumer warps, 2 
 using TmaCfgC = TmaCfg<31, 4, 7936, 1>;      // 1 CTA/SM, 31 consumer warps, 124 KB
 using TmaCfgD = TmaCfg<16, 3, 8192, 2, 2>;   // B with two float4 in flight per thread
 using TmaCfgE = TmaCfg<12, 4, 6144, 2>;      // 2 CTAs/SM, 24 consumer warps, 2 x 96 KB
+using TmaCfgH = TmaCfg<12, 2, 6144, 3>;      // 3 CTAs/SM, 36 consumer warps, 3 x 48 KB
+using TmaCfgI = TmaCfg<8, 3, 4096, 4>;       // 4 CTAs/SM, 32 consumer warps, 4 x 48 KB
 
 template <int ALG, class CFG>
 struct OpNormalF32 {
@@ -101,15 +103,15 @@ struct OpNormalF32 {
             const float x[4] = {a.x, a.y, a.z, a.w};
             bool ok = true;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= 1.17549435e-38f);
+            for (int k = 0; k < 4; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= fast_vv_min_f32<ALG>());
             float y[4];
             if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
                 for (int k = 0; k < 4; k += 2) {
                     const float oa = __fsub_rn(1.0f, x[k]), ob = __fsub_rn(1.0f, x[k + 1]);
                     const float2 lz = neg_log2x_f32x2(fminf(x[k], oa), fminf(x[k + 1], ob));
-                    y[k] = apply_sign_f32(rat32<ALG>(lz.x), x[k], oa);
-                    y[k + 1] = apply_sign_f32(rat32<ALG>(lz.y), x[k + 1], ob);
+                    y[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.x), x[k], oa);
+                    y[k + 1] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.y), x[k + 1], ob);
                 }
             } else {
 #pragma unroll
@@ -134,8 +136,9 @@ struct OpNormalF32Pipe {
     }
     QM_DEV static bool normal(const float4 a)
     {
-        return (fminf(a.x, __fsub_rn(1.0f, a.x)) >= 1.17549435e-38f) & (fminf(a.y, __fsub_rn(1.0f, a.y)) >= 1.17549435e-38f) &
-               (fminf(a.z, __fsub_rn(1.0f, a.z)) >= 1.17549435e-38f) & (fminf(a.w, __fsub_rn(1.0f, a.w)) >= 1.17549435e-38f);
+        constexpr float m = fast_vv_min_f32<ALG>();
+        return (fminf(a.x, __fsub_rn(1.0f, a.x)) >= m) & (fminf(a.y, __fsub_rn(1.0f, a.y)) >= m) &
+               (fminf(a.z, __fsub_rn(1.0f, a.z)) >= m) & (fminf(a.w, __fsub_rn(1.0f, a.w)) >= m);
     }
     QM_DEV void tile(float *t, int ctid, int nct) const
     {
@@ -213,7 +216,7 @@ k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, in
         }
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 2 * V; ++k) ok &= (fmin(x[k], __dadd_rn(1.0, -x[k])) >= 2.2250738585072014e-308);
+        for (int k = 0; k < 2 * V; ++k) ok &= (fmin(x[k], __dadd_rn(1.0, -x[k])) >= fast_vv_min_f64<ALG>());
         double y[2 * V];
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
@@ -262,10 +265,10 @@ k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned
                 for (int k = 0; k < 4; ++k) { uu[k] = u01_f32(ws[k]); om[k] = __fsub_rn(1.0f, uu[k]); }
                 const float2 l01 = neg_log2x_f32x2(fminf(uu[0], om[0]), fminf(uu[1], om[1]));
                 const float2 l23 = neg_log2x_f32x2(fminf(uu[2], om[2]), fminf(uu[3], om[3]));
-                r[0] = apply_sign_f32(rat32<ALG>(l01.x), uu[0], om[0]);
-                r[1] = apply_sign_f32(rat32<ALG>(l01.y), uu[1], om[1]);
-                r[2] = apply_sign_f32(rat32<ALG>(l23.x), uu[2], om[2]);
-                r[3] = apply_sign_f32(rat32<ALG>(l23.y), uu[3], om[3]);
+                r[0] = apply_sign_f32(rat32<fast_alg<ALG>()>(l01.x), uu[0], om[0]);
+                r[1] = apply_sign_f32(rat32<fast_alg<ALG>()>(l01.y), uu[1], om[1]);
+                r[2] = apply_sign_f32(rat32<fast_alg<ALG>()>(l23.x), uu[2], om[2]);
+                r[3] = apply_sign_f32(rat32<fast_alg<ALG>()>(l23.y), uu[3], om[3]);
             }
             const int64_t i = 4 * b;
             if (vec && i + 3 < n) {
@@ -331,14 +334,15 @@ k_antithetic_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, 
         const float x[4] = {a.x, a.y, a.z, a.w};
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ok &= (x[k] >= 1.17549435e-38f) & (x[k] <= 1.0f);
+        // v = -log u < vc for the tail composite: u > e^-37 = 8.5e-17
+        for (int k = 0; k < 4; ++k) ok &= (x[k] >= (ALG == ALG_BREAKLESS_TAIL ? 8.6e-17f : 1.17549435e-38f)) & (x[k] <= 1.0f);
         float y[4];
         if (__all_sync(0xffffffffu, ok)) {
             // -log u: eadj = -1 cancels the factor 2 of neg_log2x
             const float2 l01 = neg_log2x_f32x2(x[0], x[1], -1);
             const float2 l23 = neg_log2x_f32x2(x[2], x[3], -1);
-            y[0] = fabsf(rat32<ALG>(l01.x)); y[1] = fabsf(rat32<ALG>(l01.y));
-            y[2] = fabsf(rat32<ALG>(l23.x)); y[3] = fabsf(rat32<ALG>(l23.y));
+            y[0] = fabsf(rat32<fast_alg<ALG>()>(l01.x)); y[1] = fabsf(rat32<fast_alg<ALG>()>(l01.y));
+            y[2] = fabsf(rat32<fast_alg<ALG>()>(l23.x)); y[3] = fabsf(rat32<fast_alg<ALG>()>(l23.y));
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k) y[k] = anti_f32_careful<ALG>(x[k]);
@@ -458,7 +462,7 @@ QM_DEV double exp2n_f64(double v)
 {
     const double a = fabs(v);
     double mag;
-    if (a < 1099511627776.0) {
+    if (a < 1099511627776.0 || (ALG == ALG_BREAKLESS_TAIL && a < __longlong_as_double(0x7ff0000000000000LL))) {
         mag = rat64<ALG>(dd{a, 0.0});
     } else if (a == __longlong_as_double(0x7ff0000000000000LL)) {
         mag = a;

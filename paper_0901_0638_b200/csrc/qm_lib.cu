@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/qm.h"
@@ -97,7 +98,7 @@ char tma_cfg()
     static char c = 0;
     if (!c) {
         const char *e = getenv("QM_TMA_CFG");
-        c = (e && e[0] >= 'A' && e[0] <= 'G') ? e[0] : 'B';
+        c = (e && e[0] >= 'A' && e[0] <= 'I') ? e[0] : 'B';
     }
     return c;
 }
@@ -112,6 +113,8 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
     case 'E': return launch_stream_f32<TmaCfgE>(k_normal_f32_tma<ALG, TmaCfgE>, k_normal_f32<ALG>, u, z, n, s);
     case 'F': return launch_stream_f32<TmaCfgB>(k_normal_f32_tma_pipe<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
     case 'G': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma_pipe<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
+    case 'H': return launch_stream_f32<TmaCfgH>(k_normal_f32_tma<ALG, TmaCfgH>, k_normal_f32<ALG>, u, z, n, s);
+    case 'I': return launch_stream_f32<TmaCfgI>(k_normal_f32_tma<ALG, TmaCfgI>, k_normal_f32<ALG>, u, z, n, s);
     default: return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
     }
 }
@@ -120,6 +123,22 @@ template <int ALG>
 qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
 {
     return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
+}
+
+#define QM_ALG_LAST QM_BREAKLESS_TAIL
+
+bool breakless_family(qm_algorithm a) { return a == QM_BREAKLESS || a == QM_BREAKLESS77 || a == QM_BREAKLESS_TAIL; }
+
+// f(std::integral_constant<int, ALG>) for the breakless family, else QM_EUNSUPPORTED
+template <typename F>
+qm_status with_breakless(qm_algorithm a, F f)
+{
+    switch (a) {
+    case QM_BREAKLESS: return f(std::integral_constant<int, ALG_BREAKLESS>{});
+    case QM_BREAKLESS77: return f(std::integral_constant<int, ALG_BREAKLESS77>{});
+    case QM_BREAKLESS_TAIL: return f(std::integral_constant<int, ALG_BREAKLESS_TAIL>{});
+    default: return QM_EUNSUPPORTED;
+    }
 }
 
 }  // namespace
@@ -145,53 +164,49 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
 {
     if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;
     if (p != QM_F32 && p != QM_F64) return QM_EINVAL;
-    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
+    if (alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int vec = aligned16(u) && aligned16(z);
-    if (p == QM_F32) {
-        if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
-        if (alg == QM_BREAKLESS) return normal_f32<ALG_BREAKLESS>((const float *)u, (float *)z, n, s);
-        return normal_f32<ALG_BREAKLESS77>((const float *)u, (float *)z, n, s);
-    }
-    const int g = grid_for(n, kThreads * 4, 8);
+    if (p == QM_F32)
+        return with_breakless(alg, [&](auto A) { return normal_f32<decltype(A)::value>((const float *)u, (float *)z, n, s); });
+    const double *ud = (const double *)u;
+    double *zd = (double *)z;
     switch (alg) {
-    case QM_BREAKLESS:
-        k_normal_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n, vec); break;
-    case QM_BREAKLESS77:
-        k_normal_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n, vec); break;
-    case QM_AS241:
-        k_branchy_f64<ALG_AS241><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
-    case QM_ACKLAM:
-        k_branchy_f64<ALG_ACKLAM><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
+    case QM_AS241: k_branchy_f64<ALG_AS241><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n); return launched();
+    case QM_ACKLAM: k_branchy_f64<ALG_ACKLAM><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n); return launched();
     case QM_ACKLAM_REFINED:
-        k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>((const double *)u, (double *)z, n); break;
+        k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n);
+        return launched();
+    default: break;
     }
-    return launched();
+    const int g = grid_for(n, kThreads * 2, 8);
+    return with_breakless(alg, [&](auto A) {
+        k_normal_f64<decltype(A)::value><<<g, kThreads, 0, s>>>(ud, zd, n, vec);
+        return launched();
+    });
 }
 
 qm_status qm_normal_antithetic(const void *u, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
 {
     if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;
-    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
-    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (!breakless_family(alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     if (p == QM_F32) {
         const int vec = aligned16(u) && aligned16(z);
         const int g = grid_for(n, kThreads * 4, 8);
-        if (alg == QM_BREAKLESS)
-            k_antithetic_f32<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
-        else
-            k_antithetic_f32<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
-    } else {
-        const int g = grid_for(n, kThreads, 8);
-        if (alg == QM_BREAKLESS)
-            k_antithetic_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n);
-        else
-            k_antithetic_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n);
+        return with_breakless(alg, [&](auto A) {
+            k_antithetic_f32<decltype(A)::value><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+            return launched();
+        });
     }
-    return launched();
+    const int g = grid_for(n, kThreads, 8);
+    return with_breakless(alg, [&](auto A) {
+        k_antithetic_f64<decltype(A)::value><<<g, kThreads, 0, s>>>((const double *)u, (double *)z, n);
+        return launched();
+    });
 }
 
 static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_algorithm alg,
@@ -199,6 +214,9 @@ static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_
 {
     cudaStream_t s = (cudaStream_t)stream;
     const int vec = aligned16(z);
+    // on the odd grid v < 17 (fp32) / 37 (fp64) < vc: the tail composite is the
+    // plain rational there, so QM_BREAKLESS_TAIL runs the QM_BREAKLESS kernel
+    if (alg == QM_BREAKLESS_TAIL) alg = QM_BREAKLESS;
     if (p == QM_F32) {
         const int g = grid_for((n + 3) / 4, kThreads * 2, 8);
         if (mode == 0) k_philox_f32<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
@@ -224,8 +242,8 @@ qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
                            uint64_t counter_offset, void *stream)
 {
     if (n < 0 || (n > 0 && z == nullptr) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
-    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
-    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (!breakless_family(alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     return philox_launch(z, n, p, 1, alg, seed, counter_offset, stream);
 }
@@ -233,21 +251,17 @@ qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
 qm_status qm_recycle_exp_to_normal(const void *v, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
 {
     if (n < 0 || bad_ptrs(v, z, n)) return QM_EINVAL;
-    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
-    if (alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if ((p != QM_F32 && p != QM_F64) || alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (!breakless_family(alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (p == QM_F32) {
-        if (alg == QM_BREAKLESS) return exp2n_f32<ALG_BREAKLESS>((const float *)v, (float *)z, n, s);
-        return exp2n_f32<ALG_BREAKLESS77>((const float *)v, (float *)z, n, s);
-    } else {
-        const int g = grid_for(n, kThreads, 8);
-        if (alg == QM_BREAKLESS)
-            k_exp2n_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>((const double *)v, (double *)z, n);
-        else
-            k_exp2n_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((const double *)v, (double *)z, n);
-    }
-    return launched();
+    if (p == QM_F32)
+        return with_breakless(alg, [&](auto A) { return exp2n_f32<decltype(A)::value>((const float *)v, (float *)z, n, s); });
+    const int g = grid_for(n, kThreads, 8);
+    return with_breakless(alg, [&](auto A) {
+        k_exp2n_f64<decltype(A)::value><<<g, kThreads, 0, s>>>((const double *)v, (double *)z, n);
+        return launched();
+    });
 }
 
 qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p, double nu, int K,
@@ -347,8 +361,8 @@ thread_local HostPipe g_pipe;
 qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, qm_precision p, qm_algorithm alg)
 {
     if (n < 0 || bad_ptrs(u_host, z_host, n) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
-    if (alg < QM_BREAKLESS || alg > QM_ACKLAM_REFINED) return QM_EINVAL;
-    if (p == QM_F32 && alg != QM_BREAKLESS && alg != QM_BREAKLESS77) return QM_EUNSUPPORTED;
+    if (alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (p == QM_F32 && !breakless_family(alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     const size_t es = (p == QM_F32) ? 4 : 8;
     const int64_t chunk = (int64_t)1 << 24;                 // elements per pipeline stage

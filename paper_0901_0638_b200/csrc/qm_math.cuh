@@ -148,7 +148,7 @@ QM_DEV float2 neg_log2x_f32x2(float vva, float vvb, int eadj = 0)
 
 // |z P(z)/Q(z)| for the fp32 formulas: coefficients float-rounded, evaluated in
 // FP64 (N coefficients each), rcp seed + one quotient correction, one rounding.
-template <int N>
+template <int N, bool CORRECT = true>
 QM_DEV float rational_f32path(float z, const double *P, const double *Q)
 {
     const double zd = (double)z;
@@ -158,7 +158,10 @@ QM_DEV float rational_f32path(float z, const double *P, const double *Q)
         p = __fma_rn(p, zd, P[i]);
         q = __fma_rn(q, zd, Q[i]);
     }
+    // MUFU.RCP64H seed + one residual correction.  Measured on B200 over the whole
+    // fp32 grid: without the correction (2 DFMA) the map is 8 % faster but 16.9 ulp off.
     const double r = rcp_approx_f64(q);
+    if (!CORRECT) return (float)__dmul_rn(__dmul_rn(zd, p), r);
     double t = __dmul_rn(p, r);
     const double e = __fma_rn(-q, t, p);
     t = __fma_rn(e, r, t);
@@ -258,12 +261,37 @@ QM_DEV double apply_sign_f64(double mag, double u, double omu)
 
 // ----------------------------------------------------- breakless quantiles
 // Algorithm ids for templates (mirror qm_algorithm)
-enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1 };
+// ALG_BREAKLESS_TAIL (row f2): the breakless rational for v < vc and the §5.1
+// supplementary tail model beyond; vc = 37 for App C and
+// 86.75 for App D (reading R23).  Its fast path is ALG_BREAKLESS: the warp vote
+// sends a warp with any v >= vc to the careful path.
+enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5 };
+#define QM_VC_F32 37.0f
+#define QM_VC_F64 86.75
+
+template <int ALG> __host__ __device__ constexpr int fast_alg() { return ALG == ALG_BREAKLESS_TAIL ? ALG_BREAKLESS : ALG; }
+// smallest vv = min(u, 1-u) of the fast path: normal numbers; for the tail
+// composite also v = -log(2 vv) < vc (e^-37/2 = 4.2665e-17, e^-86.75/2 = 1.0566e-38)
+template <int ALG> __host__ __device__ constexpr float fast_vv_min_f32()
+{
+    return ALG == ALG_BREAKLESS_TAIL ? 4.3e-17f : 1.17549435e-38f;
+}
+template <int ALG> __host__ __device__ constexpr double fast_vv_min_f64()
+{
+    return ALG == ALG_BREAKLESS_TAIL ? 1.1e-38 : 2.2250738585072014e-308;
+}
+
+QM_DEV double tail_model_q(double v);   // qm_dd.cuh
+QM_DEV double tail_model_q_dd(dd v);    // qm_dd.cuh
 
 template <int ALG>
 QM_DEV float rat32(float z)
 {
     if (ALG == ALG_BREAKLESS77) return rational_f32path<8>(z, kA77P_f, kA77Q_f);
+    if (ALG == ALG_BREAKLESS_TAIL) {
+        const float r = rational_f32path<6>(z, kC55P, kC55Q);
+        return (z < QM_VC_F32) ? r : (float)tail_model_q((double)z);
+    }
     return rational_f32path<6>(z, kC55P, kC55Q);
 }
 
@@ -271,6 +299,8 @@ template <int ALG>
 QM_DEV double rat64(dd z)
 {
     if (ALG == ALG_BREAKLESS77) return rational_dd<8, 7>(z, kA77P_d, kA77Q_d);
+    if (ALG == ALG_BREAKLESS_TAIL)
+        return (z.hi < QM_VC_F64) ? rational_dd<14, 10>(z, kD13P, kD13Q) : tail_model_q_dd(z);
     // compensating the last 10 of 13 Horner steps is enough: 0.65 ulp max over
     // 2^21 grid + tail-stratified inputs in emulation (all 13: 0.53; 9: 1.20)
     return rational_dd<14, 10>(z, kD13P, kD13Q);
@@ -282,7 +312,7 @@ QM_DEV float nq_f32_fast(float u)
 {
     const float omu = __fsub_rn(1.0f, u);
     const float vv = fminf(u, omu);
-    return apply_sign_f32(rat32<ALG>(neg_log2x_f32(vv, 0)), u, omu);
+    return apply_sign_f32(rat32<fast_alg<ALG>()>(neg_log2x_f32(vv, 0)), u, omu);
 }
 
 // every input: subnormal vv pre-scaled by 2^24; 0/1 -> -+inf; else NaN
@@ -304,7 +334,7 @@ QM_DEV double nq_f64_fast(double u)
 {
     const double omu = __dadd_rn(1.0, -u);
     const double vv = fmin(u, omu);
-    return apply_sign_f64(rat64<ALG>(neg_log2x_dd(vv, 0)), u, omu);
+    return apply_sign_f64(rat64<fast_alg<ALG>()>(neg_log2x_dd(vv, 0)), u, omu);
 }
 
 template <int ALG>
