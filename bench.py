@@ -248,6 +248,29 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     return out
 
 
+def dist_variants(torch, dist, rank, world, steps=5, warmup=2):
+    """Config 4 (2^30 fp64 normals -> Student-t nu=5 -> moments) and config 5
+    (2^34-sample exponential-base call sweep) over all ranks, each step ending
+    with the NCCL all-reduce of the row matrix and the fixed-order reduction;
+    time = max over ranks.  Results are bit-identical for any number of GPUs."""
+    from paper_0901_0638_b200 import shard as S
+    out = {}
+    strikes = list(np.linspace(50, 150, 17))
+
+    def run(name, fn, n_total):
+        ms = max_over_ranks(time_steps(fn, steps, warmup, dist), dist) / steps
+        r = fn()
+        out[name] = {"gsamples_s": n_total / (ms / 1e3) / 1e9, "ms": ms, "n": n_total, "n_gpus": world,
+                     "scaling": "strong", "collective": "all_reduce(SUM) of the fixed-chunk row matrix (NCCL)",
+                     "result": [float(x) for x in (r[0] if isinstance(r, tuple) else r).flatten()[:4].cpu()]}
+
+    run("dist_student_moments_f64_nu5_2^30",
+        lambda: S.student_moments(1 << 30, 5.0, 16, 4.6506, SEED, rank, world)[0], 1 << 30)
+    run("dist_mc_call_sweep_2^34_17K",
+        lambda: S.mc_call_sweep(1 << 34, SEED, 100.0, 0.05, 0.2, 1.0, strikes, rank, world), 1 << 34)
+    return out
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args.gpus)
@@ -315,9 +338,16 @@ def run_ours(args):
                          f"2^28) -> the same formula (App C, float-rounded coefficients) in long double, "
                          f"{dt:.1f} s wall on {threads} threads"}
 
+    # configs 4 and 5 across the ranks: fixed global work split by Philox counter
+    # ranges, one NCCL all-reduce of the fixed-chunk sum rows (strong scaling)
+    dvar = None
+    if not args.no_variants:
+        dvar = dist_variants(torch, dist, rank, world)
+
     var = None
     if rank == 0 and not args.no_variants:
         var = variants(Q, torch, peaks)
+        var.update(dvar)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
