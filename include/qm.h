@@ -158,6 +158,39 @@ int64_t   qm_mc_row_count(int64_t n);
 qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset, const qm_mc_params *params,
                               double *rows, void *stream);
 
+/* Exponential-base recycling into hyperbolic and variance-gamma samples (row f1;
+ * §4).  The base is the two-sided exponential of P:315-321 with the
+ * target's masses p+-  and rates a-b (right), a+b (left);
+ * the map Q(v) = F^-1(F0(v)) solves the Recycling ODE of P:330-345.
+ *  - qm_exp_target_table builds the map for one parameter set into a
+ *    caller-owned DEVICE buffer of QM_RODE_TABLE_DOUBLES doubles: host setup
+ *    (masses by quadrature; the RODE integrated in long double backward from
+ *    an anchor at base probability e^-40, where Q is fixed by its definition,
+ *    down to v = 0 -- forward integration is exponentially ill-conditioned),
+ *    then a synchronous copy.  params: hyperbolic {alpha, beta, delta}
+ *    (alpha > |beta|, delta > 0); VG {lambda, alpha, beta} with integer
+ *    1 <= lambda <= 9 (half-integer Bessel orders; lambda = 1 is the identity,
+ *    P:395).  Otherwise QM_EINVAL / QM_EUNSUPPORTED (non-integer lambda).
+ *  - qm_recycle_exp_to_hyperbolic / qm_recycle_exp_to_vg: x[i] = Q(v[i]) for
+ *    base samples v (cubic Hermite in a table of 8193 nodes per side; linear
+ *    beyond base probability e^-40).  +-0, +-inf, NaN pass through.
+ *  - qm_exp_base_quantile: v[i] = Q0(u[i]) of P:322-329.
+ *  - qm_exp_target_philox: fused Philox (qm_philox_uniform layout) -> Q0 -> Q.
+ * Accuracy (the method's, against the exact map): ~1e-12 relative. */
+#define QM_RODE_TABLE_DOUBLES (24 + 4 * (8192 + 1))
+typedef enum { QM_TARGET_HYPERBOLIC = 1, QM_TARGET_VG = 2 } qm_target;
+qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev);
+qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p,
+                                       const double *table_dev, void *stream);
+qm_status qm_recycle_exp_to_vg(const void *v, void *x, int64_t n, qm_precision p,
+                               const double *table_dev, void *stream);
+qm_status qm_exp_base_quantile(const void *u, void *v, int64_t n, qm_precision p,
+                               const double *table_dev, void *stream);
+qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double *table_dev,
+                               uint64_t seed, uint64_t counter_offset, void *stream);
+/* the same table in HOST memory (diagnostics: header + nodes, see qm_rode_params.h) */
+int qm_rode_table_host(int kind, const double *params, double *table);
+
 /* End-to-end variant of qm_normal_quantile on HOST buffers: copies u in,
  * computes, copies z out, overlapping the three in chunks on library-owned
  * streams and pinned/device staging buffers (allocated once per thread and

@@ -27,7 +27,7 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 _SO = _HERE / "liboracle.so"
-_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_mc.c", "orc_tail.c"]
+_SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_mc.c", "orc_tail.c", "orc_rode.c"]
 
 # formula ids of the oracle (local to the oracle; the product has its own enum)
 C55, A77, D13 = 55, 77, 13
@@ -86,6 +86,9 @@ def lib():
             "orc_moments_f32": (None, [P, i64, i32, P]),
             "orc_mc_call": (None, [i64, u64, u64, dbl, dbl, dbl, dbl, P, i32, P]),
             "orc_normal_breakless_tail": (i32, [P, P, i64, i32, i32, dbl]),
+            "orc_target_masses": (i32, [i32, P, P]),
+            "orc_target_density": (i32, [i32, P, P, P, i64]),
+            "orc_recycle_exp_to_target": (i32, [i32, P, P, P, i64]),
             "orc_exp_to_normal_tail": (i32, [P, P, i64, i32, i32, dbl]),
         }
         for name, (res, args) in sig.items():
@@ -192,6 +195,29 @@ def normal_breakless_tail(u, formula: int, prec: int, vc: float) -> np.ndarray:
     """Composite of row f2: rational for v < vc, the §5.1 tail model beyond (orc_tail.c)."""
     u = _in(u); o = np.empty(u.shape, np.longdouble)
     _chk(lib().orc_normal_breakless_tail(_p(u), _p(o), u.size, formula, prec, vc))
+    return o
+
+
+HYPERBOLIC, VG = 1, 2
+
+
+def target_masses(kind: int, params):
+    """(p-, p+, Z) of the hyperbolic (params alpha, beta, delta) or VG (lambda, alpha, beta) target."""
+    p = _in(params); o = np.zeros(3, np.longdouble)
+    _chk(lib().orc_target_masses(kind, _p(p), _p(o)))
+    return o
+
+
+def target_density(kind: int, params, x) -> np.ndarray:
+    p = _in(params); x = _in(x); o = np.empty(x.shape, np.longdouble)
+    _chk(lib().orc_target_density(kind, _p(p), _p(x), _p(o), x.size))
+    return o
+
+
+def recycle_exp_to_target(kind: int, params, v) -> np.ndarray:
+    """Q(v) = F^-1(F0(v)) by definition (quadrature + bracketed Newton on the tail mass)."""
+    p = _in(params); v = _in(v); o = np.empty(v.shape, np.longdouble)
+    _chk(lib().orc_recycle_exp_to_target(kind, _p(p), _p(v), _p(o), v.size))
     return o
 
 

@@ -1,0 +1,155 @@
+/*
+ * orc_rode.c -- ORACLE (test infrastructure only; see orc.h).
+ *
+ * recycling two-sided exponential samples into
+ * hyperbolic (§4.1) and variance-gamma (§4.2) samples.
+ * The oracle states the map by its DEFINITION: Q(v) = F^-1(F0(v)), with
+ *   base f0(x) = p+ (a-b) e^{-(a-b)x} (x > 0), p- (a+b) e^{(a+b)x} (x < 0)
+ *   hyperbolic f(x) ~ exp(-a sqrt(d^2 + x^2) + b x)
+ *   VG (integer lambda = m+1 >= 1; reading R25): f(x) ~ e^{bx} |x|^{lambda-1/2} K_{lambda-1/2}(a|x|)
+ *      = e^{bx - a|x|} sum_{k=0}^{m} (m+k)!/(k!(m-k)!) (2a)^{-k} |x|^{m-k}   (K half-integer, A&S 10.2.15)
+ * p+- = target masses of x > 0 / x < 0, computed here by
+ * adaptive Gauss-Kronrod (7-15) quadrature of the unnormalised density; the
+ * tail masses by the same quadrature; Q by bracketed bisection on the TAIL
+ * probability (never 1 - F):  v >= 0: Fbar(Q) = p+ e^{-(a-b) v};
+ *                             v <  0: F(Q)    = p- e^{(a+b) v}.
+ * Long double throughout.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <float.h>
+#include "orc.h"
+
+typedef struct { int kind; ld a, b, d; int m; } tgt_t;   /* kind 1 hyperbolic, 2 VG */
+
+static ld dens_u(const tgt_t *t, ld x)                   /* unnormalised density */
+{
+    if (t->kind == 1) return expl(-t->a * sqrtl(t->d * t->d + x * x) + t->b * x);
+    ld ax = fabsl(x), s = 0.0L, fact_mk = 1.0L;
+    /* sum_{k=0}^{m} (m+k)!/(k!(m-k)!) (2a)^-k |x|^{m-k} */
+    for (int k = 0; k <= t->m; ++k) {
+        ld c = 1.0L;
+        for (int j = t->m - k + 1; j <= t->m + k; ++j) c *= (ld)j;      /* (m+k)!/(m-k)! */
+        for (int j = 2; j <= k; ++j) c /= (ld)j;                          /* /k! */
+        s += c * powl(2.0L * t->a, -(ld)k) * powl(ax, (ld)(t->m - k));
+    }
+    (void)fact_mk;
+    return expl(t->b * x - t->a * ax) * s;
+}
+
+/* Gauss-Kronrod 7-15 on [lo, hi], adaptive (absolute tolerance relative to the running total) */
+static const ld XK[8] = {0.991455371120812639206854697526329L, 0.949107912342758524526189684047851L,
+                         0.864864423359769072789712788640926L, 0.741531185599394439863864773280788L,
+                         0.586087235467691130294144845693013L, 0.405845151377397166906606412076961L,
+                         0.207784955007898467600689403773245L, 0.0L};
+static const ld WK[8] = {0.022935322010529224963732008058970L, 0.063092092629978553290700663189204L,
+                         0.104790010322250183839876322541518L, 0.140653259715525918745189590510238L,
+                         0.169004726639267902826583426598550L, 0.190350578064785409913256402421014L,
+                         0.204432940075298892414161999234649L, 0.209482141084727828012999174891714L};
+static const ld WG[4] = {0.129484966168869693270611432679082L, 0.279705391489276667901467771423780L,
+                         0.381830050505118944950369775488975L, 0.417959183673469387755102040816327L};
+
+static ld gk15(const tgt_t *t, ld lo, ld hi, ld *err)
+{
+    ld c = 0.5L * (lo + hi), h = 0.5L * (hi - lo);
+    ld fc = dens_u(t, c), rk = WK[7] * fc, rg = WG[3] * fc;
+    for (int j = 0; j < 7; ++j) {
+        ld f1 = dens_u(t, c - h * XK[j]), f2 = dens_u(t, c + h * XK[j]);
+        rk += WK[j] * (f1 + f2);
+        if (j % 2 == 1) rg += WG[j / 2] * (f1 + f2);
+    }
+    *err = fabsl((rk - rg) * h);
+    return rk * h;
+}
+
+static ld integ(const tgt_t *t, ld lo, ld hi, ld tol, int depth)
+{
+    ld e, r = gk15(t, lo, hi, &e);
+    /* stop at the tolerance or at long double's rounding floor of the panel */
+    if (e <= tol || e <= 8.0L * LDBL_EPSILON * fabsl(r) || depth > 24) return r;
+    ld m = 0.5L * (lo + hi);
+    return integ(t, lo, m, 0.5L * tol, depth + 1) + integ(t, m, hi, 0.5L * tol, depth + 1);
+}
+
+/* integral over [x, inf) (right) or (-inf, x] (left), panels of 1/rate out to 120/rate */
+static ld tail_int(const tgt_t *t, ld x, int right)
+{
+    ld rate = right ? (t->a - t->b) : (t->a + t->b);
+    ld w = 1.0L / rate, s = 0.0L, scale = dens_u(t, x) * w + 1e-4900L;
+    for (int k = 0; k < 160; ++k) {
+        ld lo = right ? x + k * w : x - (k + 1) * w, hi = lo + w;
+        ld p = integ(t, lo, hi, 1e-21L * scale, 0);
+        s += p;
+        if (p < 1e-24L * s) break;
+    }
+    return s;
+}
+
+static void masses(const tgt_t *t, ld *pm, ld *pp, ld *Z)
+{
+    ld r = tail_int(t, 0.0L, 1), l = tail_int(t, 0.0L, 0);
+    *Z = r + l; *pp = r / *Z; *pm = l / *Z;
+}
+
+static int make_tgt(int kind, const double *par, tgt_t *t)
+{
+    t->kind = kind;
+    if (kind == 1) { t->a = par[0]; t->b = par[1]; t->d = par[2]; t->m = 0; return !(par[0] > fabs(par[1]) && par[2] > 0); }
+    if (kind == 2) {
+        t->m = (int)par[0] - 1; t->a = par[1]; t->b = par[2]; t->d = 0;
+        return !(par[0] >= 1 && par[0] == (int)par[0] && par[1] > fabs(par[2]));
+    }
+    return 1;
+}
+
+int orc_target_masses(int kind, const double *par, ld *out /* p-, p+, Z */)
+{
+    tgt_t t;
+    if (make_tgt(kind, par, &t)) return -1;
+    masses(&t, &out[0], &out[1], &out[2]);
+    return 0;
+}
+
+/* normalised density (for the slope pins) */
+int orc_target_density(int kind, const double *par, const double *x, ld *out, int64_t n)
+{
+    tgt_t t; ld pm, pp, Z;
+    if (make_tgt(kind, par, &t)) return -1;
+    masses(&t, &pm, &pp, &Z);
+    for (int64_t i = 0; i < n; ++i) out[i] = dens_u(&t, (ld)x[i]) / Z;
+    return 0;
+}
+
+/* Q(v) = F^-1(F0(v)) for base samples v (two-sided exponential with the target's split) */
+int orc_recycle_exp_to_target(int kind, const double *par, const double *v, ld *out, int64_t n)
+{
+    tgt_t t; ld pm, pp, Z;
+    if (make_tgt(kind, par, &t)) return -1;
+    masses(&t, &pm, &pp, &Z);
+    const ld rr = t.a - t.b, rl = t.a + t.b;
+    for (int64_t i = 0; i < n; ++i) {
+        ld vi = (ld)v[i];
+        if (isnan(vi)) { out[i] = NAN; continue; }
+        if (isinf(vi)) { out[i] = vi; continue; }
+        if (vi == 0.0L) { out[i] = vi; continue; }
+        int right = vi > 0.0L;
+        /* target tail mass (normalised) */
+        ld target = right ? pp * expl(-rr * vi) : pm * expl(rl * vi);
+        /* bracket: |Q| in [0, hi] */
+        ld lo = 0.0L, hi = 1.0L;
+        while (tail_int(&t, right ? hi : -hi, right) / Z > target && hi < 1e6L) { lo = hi; hi *= 2.0L; }
+        /* bracketed Newton on g(q) = tail(q) - target, g' = -f(q) (bisection if it leaves the bracket) */
+        ld q = 0.5L * (lo + hi);
+        for (int it = 0; it < 200; ++it) {
+            ld x = right ? q : -q;
+            ld g = tail_int(&t, x, right) / Z - target;
+            if (g > 0.0L) lo = q; else hi = q;
+            ld qn = q + g / (dens_u(&t, x) / Z);
+            if (!(qn > lo && qn < hi)) qn = 0.5L * (lo + hi);
+            if (fabsl(qn - q) <= 4.0L * LDBL_EPSILON * qn || hi - lo <= 4.0L * LDBL_EPSILON * hi) { q = qn; break; }
+            q = qn;
+        }
+        out[i] = right ? q : -q;
+    }
+    return 0;
+}

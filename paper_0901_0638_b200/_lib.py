@@ -16,6 +16,8 @@ QM_F32, QM_F64 = 1, 2
 QM_BREAKLESS, QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED, QM_BREAKLESS_TAIL = 0, 1, 2, 3, 4, 5
 QM_MOMENT_CHUNK = 65536
 QM_MC_CHUNK = 1 << 20
+QM_TARGET_HYPERBOLIC, QM_TARGET_VG = 1, 2
+QM_RODE_TABLE_DOUBLES = 24 + 4 * (8192 + 1)
 QM_MC_MAX_STRIKES = 32
 
 
@@ -37,6 +39,12 @@ SIGNATURES = {
     "qm_normal_philox": (_I32, [_P, _I64, _I32, _I32, _U64, _U64, _P]),
     "qm_recycle_normal_to_t": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P]),
     "qm_recycle_exp_to_normal": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
+    "qm_exp_target_table": (_I32, [_I32, _P, _P]),
+    "qm_recycle_exp_to_hyperbolic": (_I32, [_P, _P, _I64, _I32, _P, _P]),
+    "qm_recycle_exp_to_vg": (_I32, [_P, _P, _I64, _I32, _P, _P]),
+    "qm_exp_base_quantile": (_I32, [_P, _P, _I64, _I32, _P, _P]),
+    "qm_exp_target_philox": (_I32, [_P, _I64, _I32, _P, _U64, _U64, _P]),
+    "qm_rode_table_host": (_I32, [_I32, _P, _P]),
     "qm_mc_row_count": (_I64, [_I64]),
     "qm_mc_european_call": (_I32, [_I64, _U64, _U64, _P, _P, _P]),
     "qm_moment_row_count": (_I64, [_I64]),

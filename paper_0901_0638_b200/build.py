@@ -32,16 +32,21 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
-    obj = HERE / "qm_student_host.o"
-    subprocess.run(["g++", "-O2", "-std=gnu++17", "-fext-numeric-literals", "-fPIC", "-c", str(CSRC / "qm_student_host.cpp"),
-                    "-o", str(obj)], check=True)
+    # host-side parameter setup (C++, long double / __float128)
+    objs = []
+    for src in sorted(CSRC.glob("*.cpp")):
+        obj = HERE / (src.stem + ".o")
+        subprocess.run(["g++", "-O2", "-std=gnu++17", "-fext-numeric-literals", "-fPIC", "-c", str(src),
+                        "-o", str(obj)], check=True)
+        objs.append(obj)
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-I", str(ROOT / "include"), str(CSRC / "qm_lib.cu"), str(obj), "-lquadmath",
+           "-I", str(ROOT / "include"), str(CSRC / "qm_lib.cu"), *map(str, objs), "-lquadmath",
            "-o", str(LIB)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    obj.unlink(missing_ok=True)
+    for o in objs:
+        o.unlink(missing_ok=True)
     return LIB
 
 

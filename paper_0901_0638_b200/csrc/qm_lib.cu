@@ -16,6 +16,7 @@
 #include "qm_student.cuh"
 #include "qm_moments.cuh"
 #include "qm_mc.cuh"
+#include "qm_rode.cuh"
 #include <cmath>
 
 using namespace qm;
@@ -281,6 +282,70 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
     const int g = grid_for(n, kThreads * 2, 8);
     if (p == QM_F64) k_student_f64<<<g, kThreads, 0, s>>>((const double *)z, (double *)t, n, sp);
     else k_student_f32<<<g, kThreads, 0, s>>>((const float *)z, (float *)t, n, sp);
+    return launched();
+}
+
+qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev)
+{
+    if (params == nullptr || table_dev == nullptr || (kind != QM_TARGET_HYPERBOLIC && kind != QM_TARGET_VG))
+        return QM_EINVAL;
+    // a valid VG with lambda not an integer in [1, 9]: unsupported (lambda < 1 is out of scope)
+    if (kind == QM_TARGET_VG && params[0] > 0.0 && params[1] > std::fabs(params[2]) &&
+        (params[0] != std::floor(params[0]) || params[0] < 1.0 || params[0] > QM_RODE_VG_MAXM + 1))
+        return QM_EUNSUPPORTED;
+    std::vector<double> tab(QM_RODE_TABLE_DOUBLES);
+    if (!rode_table_build((int)kind, params, tab.data())) return QM_EINVAL;
+    return cudaMemcpy(table_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess
+               ? QM_OK : QM_ECUDA;
+}
+
+static qm_status rode_map_launch(const void *v, void *x, int64_t n, qm_precision p, const double *tab, void *stream)
+{
+    if (n < 0 || bad_ptrs(v, x, n) || tab == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = grid_for(n, kThreads, 8);
+    if (p == QM_F64) k_rode_map<double><<<g, kThreads, 0, s>>>((const double *)v, (double *)x, n, tab);
+    else k_rode_map<float><<<g, kThreads, 0, s>>>((const float *)v, (float *)x, n, tab);
+    return launched();
+}
+
+qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p, const double *table_dev,
+                                       void *stream)
+{
+    return rode_map_launch(v, x, n, p, table_dev, stream);
+}
+
+qm_status qm_recycle_exp_to_vg(const void *v, void *x, int64_t n, qm_precision p, const double *table_dev,
+                               void *stream)
+{
+    return rode_map_launch(v, x, n, p, table_dev, stream);
+}
+
+qm_status qm_exp_base_quantile(const void *u, void *v, int64_t n, qm_precision p, const double *table_dev,
+                               void *stream)
+{
+    if (n < 0 || bad_ptrs(u, v, n) || table_dev == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = grid_for(n, kThreads, 8);
+    if (p == QM_F64) k_exp_base_quantile<double><<<g, kThreads, 0, s>>>((const double *)u, (double *)v, n, table_dev);
+    else k_exp_base_quantile<float><<<g, kThreads, 0, s>>>((const float *)u, (float *)v, n, table_dev);
+    return launched();
+}
+
+qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double *table_dev, uint64_t seed,
+                               uint64_t counter_offset, void *stream)
+{
+    if (n < 0 || (n > 0 && x == nullptr) || table_dev == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p == QM_F64)
+        k_rode_philox<double><<<grid_for((n + 1) / 2, kThreads, 8), kThreads, 0, s>>>((double *)x, n, seed,
+                                                                                       counter_offset, table_dev);
+    else
+        k_rode_philox<float><<<grid_for((n + 3) / 4, kThreads, 8), kThreads, 0, s>>>((float *)x, n, seed,
+                                                                                      counter_offset, table_dev);
     return launched();
 }
 

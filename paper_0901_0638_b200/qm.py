@@ -99,6 +99,63 @@ def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, st
     return z
 
 
+HYPERBOLIC, VG = L.QM_TARGET_HYPERBOLIC, L.QM_TARGET_VG
+
+
+def _params(p):
+    import ctypes
+    arr = (ctypes.c_double * 3)(*[float(x) for x in p])
+    return arr
+
+
+def qm_exp_target_table(kind: int, params, device=None) -> torch.Tensor:
+    """Device table of the exponential-base recycling map (hyperbolic: alpha, beta, delta;
+    VG: lambda, alpha, beta)."""
+    tab = torch.empty(L.QM_RODE_TABLE_DOUBLES, dtype=torch.float64, device=device or "cuda")
+    L.check("qm_exp_target_table", L.load().qm_exp_target_table(kind, _params(params), tab.data_ptr()))
+    return tab
+
+
+def qm_rode_table_host(kind: int, params):
+    """The same table in host memory (numpy), for diagnostics."""
+    import ctypes
+    import numpy as np
+    tab = np.zeros(L.QM_RODE_TABLE_DOUBLES, np.float64)
+    if L.load().qm_rode_table_host(kind, _params(params), tab.ctypes.data_as(ctypes.c_void_p)) != 0:
+        raise ValueError("bad target parameters")
+    return tab
+
+
+def _rode_call(name, v, table, out, stream):
+    _dev(v, "v")
+    _dev(table, "table")
+    x = _out(v, out)
+    L.check(name, getattr(L.load(), name)(v.data_ptr(), x.data_ptr(), v.numel(), _prec(v), table.data_ptr(),
+                                          _stream(stream)))
+    return x
+
+
+def qm_recycle_exp_to_hyperbolic(v: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return _rode_call("qm_recycle_exp_to_hyperbolic", v, table, out, stream)
+
+
+def qm_recycle_exp_to_vg(v: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return _rode_call("qm_recycle_exp_to_vg", v, table, out, stream)
+
+
+def qm_exp_base_quantile(u: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return _rode_call("qm_exp_base_quantile", u, table, out, stream)
+
+
+def qm_exp_target_philox(n: int, table: torch.Tensor, seed: int, counter_offset: int = 0, dtype=torch.float64,
+                         out=None, stream=None) -> torch.Tensor:
+    _dev(table, "table")
+    x = out if out is not None else torch.empty(n, dtype=dtype, device=table.device)
+    L.check("qm_exp_target_philox", L.load().qm_exp_target_philox(x.data_ptr(), n, _prec(x), table.data_ptr(), seed,
+                                                                  counter_offset, _stream(stream)))
+    return x
+
+
 def qm_mc_row_count(n: int) -> int:
     return L.load().qm_mc_row_count(n)
 

@@ -1,0 +1,83 @@
+"""GPU parity of the exponential-base recycling into hyperbolic / VG samples
+(SURVEY §8 row f1): the kernel (cubic Hermite on the RODE table) against the
+oracle's exact map Q(v) = F^-1(F0(v)).  Bar: the method's accuracy, 2e-11
+relative in fp64 (table 1e-12 + interpolation), and 2 ulp + that in fp32."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from _parity import ulp_errors
+
+pytestmark = pytest.mark.gpu
+Q = pytest.importorskip("paper_0901_0638_b200.qm")
+
+CASES = [(O.HYPERBOLIC, [1.0, 0.0, 1.0]), (O.HYPERBOLIC, [1.0, 0.5, 1.0]), (O.HYPERBOLIC, [2.0, -1.0, 0.5]),
+         (O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4])]
+
+
+def _base_samples(kind, par, n, seed=5):
+    """two-sided exponential samples with the target's split, numpy."""
+    m = O.target_masses(kind, par).astype(np.float64)
+    a, b = (par[0], par[1]) if kind == O.HYPERBOLIC else (par[1], par[2])
+    rng = np.random.default_rng(seed)
+    right = rng.uniform(size=n) < m[1]
+    e = rng.standard_exponential(n)
+    return np.where(right, e / (a - b), -e / (a + b))
+
+
+@pytest.mark.parametrize("kind,par", CASES)
+def test_recycle_exp_to_target_vs_exact_map(kind, par):
+    tab = Q.qm_exp_target_table(kind, par)
+    v = np.concatenate([_base_samples(kind, par, 400), [0.0, -0.0, 1e-12, -1e-9, 60.0, -70.0]])
+    fn = Q.qm_recycle_exp_to_hyperbolic if kind == O.HYPERBOLIC else Q.qm_recycle_exp_to_vg
+    g = fn(torch.from_numpy(v).cuda(), tab).cpu().numpy()
+    ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
+    nz = v != 0
+    rel = np.abs(g[nz] / ex[nz] - 1)
+    inside = np.abs(v[nz]) < 35.0
+    assert rel[inside].max() < 2e-11, rel.max()
+    assert rel.max() < 1e-7                       # linear extrapolation beyond base probability e^-40
+    assert g[~nz].tolist() == v[~nz].tolist() and np.array_equal(np.signbit(g[~nz]), np.signbit(v[~nz]))
+    g32 = fn(torch.from_numpy(v.astype(np.float32)).cuda(), tab).cpu().numpy()
+    ex32 = O.recycle_exp_to_target(kind, par, v.astype(np.float32).astype(np.float64))
+    assert ulp_errors(g32, ex32, np.float32).max() <= 2.0
+
+
+def test_specials_and_fused_sampler():
+    kind, par = O.HYPERBOLIC, [1.0, 0.5, 1.0]
+    tab = Q.qm_exp_target_table(kind, par)
+    v = torch.tensor([np.inf, -np.inf, np.nan], dtype=torch.float64, device="cuda")
+    g = Q.qm_recycle_exp_to_hyperbolic(v, tab).cpu().numpy()
+    assert g[0] == np.inf and g[1] == -np.inf and np.isnan(g[2])
+    # fused = Philox uniforms -> base quantile -> map, bitwise
+    n, seed = (1 << 20) + 3, 77
+    for dt in (torch.float64, torch.float32):
+        fused = Q.qm_exp_target_philox(n, tab, seed, 9, dtype=dt)
+        u = Q.qm_philox_uniform(n, seed, 9, dtype=dt)
+        unf = Q.qm_recycle_exp_to_hyperbolic(Q.qm_exp_base_quantile(u, tab), tab)
+        if dt == torch.float64:
+            assert torch.equal(fused, unf)
+        else:   # fp32: the fused kernel keeps v in double; the unfused rounds it to float
+            assert torch.allclose(fused, unf, rtol=3e-7, atol=0)
+
+
+def test_base_quantile_and_moments():
+    """Q0 of P:322-329 vs its closed form; the recycled samples' mean vs the density's."""
+    import mpmath as mp
+    kind, par = O.HYPERBOLIC, [2.0, -1.0, 0.5]
+    tab = Q.qm_exp_target_table(kind, par)
+    m = O.target_masses(kind, par).astype(np.float64)
+    u = O.philox_uniform(1 << 16, 3, 0, np.float64)
+    v = Q.qm_exp_base_quantile(torch.from_numpy(u).cuda(), tab).cpu().numpy()
+    ul = u.astype(np.longdouble)
+    ref = np.where(u < m[0], np.log(ul / m[0]) / 1.0, -np.log((1 - ul) / m[1]) / 3.0)
+    assert np.max(np.abs(v - ref.astype(np.float64)) / np.maximum(1e-300, np.abs(ref.astype(np.float64)))) < 1e-13
+    x = Q.qm_exp_target_philox(1 << 24, tab, 11, 0)
+    mp.mp.dps = 20
+    f = lambda t: mp.exp(-2.0 * mp.sqrt(0.25 + t * t) - 1.0 * t)
+    Z = mp.quad(f, [-mp.inf, 0, mp.inf])
+    mean = mp.quad(lambda t: t * f(t), [-mp.inf, 0, mp.inf]) / Z
+    var = mp.quad(lambda t: t * t * f(t), [-mp.inf, 0, mp.inf]) / Z - mean ** 2
+    se = float(mp.sqrt(var / (1 << 24)))
+    assert abs(float(x.mean()) - float(mean)) < 6 * se

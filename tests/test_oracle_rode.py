@@ -1,0 +1,124 @@
+"""Pins for the oracle's exponential-base recycling map (§4,
+P:284-395): masses p+- (P:307-314), the centre slope f0(0+)/f(0)
+(P:336), the VG lambda = 1 identity, closed-form CDFs, mpmath."""
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle as O
+from _util import ld2mp
+
+HYP = [(1.0, 0.0, 1.0), (1.0, 0.5, 1.0), (2.0, -1.0, 0.5)]
+
+
+def _mp_hyp_masses(a, b, d):
+    mp.mp.dps = 30
+    f = lambda x: mp.exp(-a * mp.sqrt(d * d + x * x) + b * x)
+    zp, zm = mp.quad(f, [0, mp.inf]), mp.quad(f, [-mp.inf, 0])
+    return zm / (zp + zm), zp / (zp + zm)
+
+
+@pytest.mark.parametrize("par", HYP)
+def test_hyperbolic_masses_vs_mpmath(par):
+    m = O.target_masses(O.HYPERBOLIC, par)
+    pm, pp = _mp_hyp_masses(*par)
+    assert abs(ld2mp(m[0]) - pm) < 1e-17 and abs(ld2mp(m[1]) - pp) < 1e-17
+    if par[1] == 0.0:
+        assert abs(float(m[0]) - 0.5) < 1e-18          # beta = 0 -> p+ = p- = 1/2 (symmetric density)
+
+
+def test_hyperbolic_centre_slope_is_K1e():
+    """alpha = delta = 1, beta = 0: Q'(0) = p+ (a-b) 2 a d K1(d g) e^{a d}/g = K1(1) e ~ 1.63615
+    (SPEC S:263)."""
+    f0 = O.target_density(O.HYPERBOLIC, [1.0, 0.0, 1.0], [0.0])[0]
+    slope = 0.5 * 1.0 / f0
+    mp.mp.dps = 30
+    assert abs(ld2mp(slope) - mp.besselk(1, 1) * mp.e) < 1e-17
+    # and the normalised density matches the closed form g/(2 a d K1(d g))
+    x = np.array([-3.0, 0.2, 1.7])
+    got = O.target_density(O.HYPERBOLIC, [1.0, 0.5, 1.0], x)
+    g = mp.sqrt(1 - 0.25)
+    for xi, gi in zip(x, got):
+        ref = g / (2 * 1.0 * 1.0 * mp.besselk(1, g)) * mp.exp(-mp.sqrt(1 + xi * xi) + 0.5 * xi)
+        assert abs(ld2mp(gi) / ref - 1) < 5e-17
+
+
+@pytest.mark.parametrize("par", HYP)
+def test_hyperbolic_map_vs_mpmath(par):
+    """Q(v) = F^-1(F0(v)) at a few v, checked by mpmath quadrature of the tail."""
+    mp.mp.dps = 30
+    a, b, d = par
+    pm, pp = _mp_hyp_masses(*par)
+    f = lambda x: mp.exp(-a * mp.sqrt(d * d + x * x) + b * x)
+    Z = mp.quad(f, [-mp.inf, 0, mp.inf])
+    v = np.array([0.3, 2.0, 8.0, -0.4, -3.0])
+    q = O.recycle_exp_to_target(O.HYPERBOLIC, par, v)
+    for vi, qi in zip(v, q):
+        qq = ld2mp(qi)
+        if vi > 0:
+            lhs, rhs = mp.quad(f, [qq, mp.inf]) / Z, pp * mp.exp(-(a - b) * vi)
+        else:
+            lhs, rhs = mp.quad(f, [-mp.inf, qq]) / Z, pm * mp.exp((a + b) * vi)
+        dens = f(qq) / Z
+        assert abs(lhs - rhs) / dens <= 1e-16 * max(1, abs(qq))          # |dQ| = |dF|/f
+
+
+def test_hyperbolic_symmetry_beta0():
+    v = np.array([0.1, 1.0, 5.0, 12.0])
+    a = O.recycle_exp_to_target(O.HYPERBOLIC, [1.0, 0.0, 1.0], v)
+    b = O.recycle_exp_to_target(O.HYPERBOLIC, [1.0, 0.0, 1.0], -v)
+    assert np.all(np.abs(a + b) <= 1e-17 * np.abs(a))
+
+
+def test_vg_lambda1_is_identity_and_masses():
+    """'if lambda = 1 the VG model is ... identical to the base, so that Q(v) = v';
+    its split is the two-sided exponential's, p+ = (a+b)/(2a)."""
+    par = [1, 2.0, 0.5]
+    m = O.target_masses(O.VG, par)
+    assert abs(float(m[1]) - 2.5 / 4.0) < 1e-18
+    v = np.array([-5.0, -0.3, 0.2, 3.0, 9.0])
+    assert np.all(np.abs(O.recycle_exp_to_target(O.VG, par, v) - v) <= 1e-17 * np.abs(v))
+
+
+def test_vg_lambda2_closed_form_cdf():
+    """lambda = 2: K_{3/2}(z) = sqrt(pi/2z) e^-z (1 + 1/z), so f ~ e^{bx - a|x|}(|x| + 1/a)
+    and the tails integrate in closed form; p+-  and Q against them."""
+    a, b = 2.0, 0.5
+    mp.mp.dps = 30
+    r, l = mp.mpf(a - b), mp.mpf(a + b)
+    # integral_q^inf e^{-r x}(x + 1/a) dx = e^{-r q}((q + 1/a)/r + 1/r^2)
+    tail_r = lambda q: mp.exp(-r * q) * ((q + 1 / mp.mpf(a)) / r + 1 / r ** 2)
+    tail_l = lambda q: mp.exp(l * q) * ((-q + 1 / mp.mpf(a)) / l + 1 / l ** 2)
+    Z = tail_r(0) + tail_l(0)
+    m = O.target_masses(O.VG, [2, a, b])
+    assert abs(ld2mp(m[1]) - tail_r(0) / Z) < 1e-18
+    for vi in (0.5, 4.0, -1.0, -6.0):
+        q = ld2mp(O.recycle_exp_to_target(O.VG, [2, a, b], [vi])[0])
+        if vi > 0:
+            err = tail_r(q) / Z - (tail_r(0) / Z) * mp.exp(-r * vi)
+            dens = mp.exp(-r * q) * (q + 1 / mp.mpf(a)) / Z
+        else:
+            err = tail_l(q) / Z - (tail_l(0) / Z) * mp.exp(l * vi)
+            dens = mp.exp(l * q) * (-q + 1 / mp.mpf(a)) / Z
+        assert abs(err) / dens <= 1e-16 * max(1, abs(q))
+
+
+# ------------------------------------------- the product's host-side table builder
+@pytest.mark.parametrize("kind,par", [(O.HYPERBOLIC, p) for p in HYP] +
+                         [(O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4])])
+def test_product_rode_table_vs_oracle(kind, par):
+    """libqm's table (RODE integrated backward in long double) at sampled nodes vs the
+    oracle's exact map; Q(0) = 0 and the centre slopes of P:336/P:344 as residuals."""
+    from paper_0901_0638_b200.qm import qm_rode_table_host
+    tab = qm_rode_table_host(kind, par)
+    N, H = 8192, 24
+    assert np.all(np.abs(tab[12:14]) < 1e-12) and np.all(np.abs(tab[14:16]) < 1e-12)
+    m = O.target_masses(kind, par)
+    assert abs(tab[8] - float(m[1])) < 1e-15 and abs(tab[9] - float(m[0])) < 1e-15
+    for side in (0, 1):
+        h = tab[2 + side]
+        nodes = tab[H + side * 2 * (N + 1):H + (side + 1) * 2 * (N + 1)].reshape(-1, 2)
+        ks = np.array([1, 37, 500, 2000, 5000, 8191])
+        v = ks * h * (1 if side == 0 else -1)
+        ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
+        assert np.abs(nodes[ks, 0] / ex - 1).max() < 1e-11
