@@ -133,6 +133,26 @@ int orc_recycle_exp_to_target(int kind, const double *par, const double *v, ld *
         if (isinf(vi)) { out[i] = vi; continue; }
         if (vi == 0.0L) { out[i] = vi; continue; }
         int right = vi > 0.0L;
+        ld rate = right ? rr : rl;
+        if (rate * fabsl(vi) < 0.5L) {
+            /* near the centre solve for the mass between 0 and Q instead (no cancellation):
+               int_0^Q f = p (1 - e^{-rate |v|}) = -p expm1(-rate |v|)                    */
+            ld target = -(right ? pp : pm) * expm1l(-rate * fabsl(vi));
+            ld lo = 0.0L, hi = 1.0L, q;
+            while (integ(&t, right ? 0.0L : -hi, right ? hi : 0.0L, 0.0L, 0) / Z < target && hi < 1e6L) { lo = hi; hi *= 2.0L; }
+            q = 0.5L * (lo + hi);
+            for (int it = 0; it < 200; ++it) {
+                ld x = right ? q : -q;
+                ld g = integ(&t, right ? 0.0L : x, right ? x : 0.0L, 0.0L, 0) / Z - target;   /* increasing in q */
+                if (g > 0.0L) hi = q; else lo = q;
+                ld qn = q - g / (dens_u(&t, x) / Z);
+                if (!(qn > lo && qn < hi)) qn = 0.5L * (lo + hi);
+                if (fabsl(qn - q) <= 4.0L * LDBL_EPSILON * qn || hi - lo <= 4.0L * LDBL_EPSILON * hi) { q = qn; break; }
+                q = qn;
+            }
+            out[i] = right ? q : -q;
+            continue;
+        }
         /* target tail mass (normalised) */
         ld target = right ? pp * expl(-rr * vi) : pm * expl(rl * vi);
         /* bracket: |Q| in [0, hi] */
