@@ -165,19 +165,23 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
  *  - qm_exp_target_table builds the map for one parameter set into a
  *    caller-owned DEVICE buffer of QM_RODE_TABLE_DOUBLES doubles: host setup
  *    (masses by quadrature; the RODE integrated in long double backward from
- *    an anchor at base probability e^-40, where Q is fixed by its definition,
- *    down to v = 0 -- forward integration is exponentially ill-conditioned),
- *    then a synchronous copy.  params: hyperbolic {alpha, beta, delta}
+ *    an anchor at base probability e^-800, where Q is fixed by its definition,
+ *    down to v = 0 -- forward integration is exponentially ill-conditioned --
+ *    and the first unit of rate*|v| redone forward from the exact centre
+ *    conditions), then a synchronous copy (~1 MB; tens of ms of host work
+ *    per parameter set).  params: hyperbolic {alpha, beta, delta}
  *    (alpha > |beta|, delta > 0); VG {lambda, alpha, beta} with integer
  *    1 <= lambda <= 9 (half-integer Bessel orders; lambda = 1 is the identity,
  *    P:395).  Otherwise QM_EINVAL / QM_EUNSUPPORTED (non-integer lambda).
  *  - qm_recycle_exp_to_hyperbolic / qm_recycle_exp_to_vg: x[i] = Q(v[i]) for
- *    base samples v (cubic Hermite in a table of 8193 nodes per side; linear
- *    beyond base probability e^-40).  +-0, +-inf, NaN pass through.
+ *    base samples v (quintic Hermite on (Q, Q', Q'') at 24577 nodes per side:
+ *    4096 on the centre rate*|v| <= 2, 16384 out to base probability e^-40,
+ *    4096 out to e^-800; linear beyond).  +-0, +-inf, NaN pass through.
  *  - qm_exp_base_quantile: v[i] = Q0(u[i]) of P:322-329.
  *  - qm_exp_target_philox: fused Philox (qm_philox_uniform layout) -> Q0 -> Q.
- * Accuracy (the method's, against the exact map): ~1e-12 relative. */
-#define QM_RODE_TABLE_DOUBLES (24 + 4 * (8192 + 1))
+ * Accuracy (the method's, against the exact map): < 2e-12 relative in fp64
+ * (worst near v = 0), correctly rounded to within 2 ulp in fp32. */
+#define QM_RODE_TABLE_DOUBLES (80 + 8 * (4096 + 16384 + 4096 + 1))
 typedef enum { QM_TARGET_HYPERBOLIC = 1, QM_TARGET_VG = 2 } qm_target;
 qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev);
 qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p,

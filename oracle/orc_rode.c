@@ -65,8 +65,12 @@ static ld gk15(const tgt_t *t, ld lo, ld hi, ld *err)
 static ld integ(const tgt_t *t, ld lo, ld hi, ld tol, int depth)
 {
     ld e, r = gk15(t, lo, hi, &e);
-    /* stop at the tolerance or at long double's rounding floor of the panel */
-    if (e <= tol || e <= 8.0L * LDBL_EPSILON * fabsl(r) || depth > 24) return r;
+    /* stop at the tolerance or at long double's rounding floor of the panel: the
+       abscissae c +- h x_j carry an absolute rounding of ~eps |c|, i.e. a relative
+       error of ~eps |c| |(log f)'| <= eps |c| (a + |b| + 1) in f, which the
+       Kronrod-Gauss difference cannot get below */
+    ld floor_rel = 8.0L * LDBL_EPSILON * (1.0L + (fabsl(lo) + fabsl(hi)) * (t->a + fabsl(t->b) + 1.0L));
+    if (e <= tol || e <= floor_rel * fabsl(r) || depth > 24) return r;
     ld m = 0.5L * (lo + hi);
     return integ(t, lo, m, 0.5L * tol, depth + 1) + integ(t, m, hi, 0.5L * tol, depth + 1);
 }
@@ -158,13 +162,15 @@ int orc_recycle_exp_to_target(int kind, const double *par, const double *v, ld *
         /* bracket: |Q| in [0, hi] */
         ld lo = 0.0L, hi = 1.0L;
         while (tail_int(&t, right ? hi : -hi, right) / Z > target && hi < 1e6L) { lo = hi; hi *= 2.0L; }
-        /* bracketed Newton on g(q) = tail(q) - target, g' = -f(q) (bisection if it leaves the bracket) */
+        /* bracketed Newton on g(q) = log tail(q) - log target, g' = -f(q)/tail(q)
+           (the log makes it quadratic from afar; bisection if it leaves the bracket) */
         ld q = 0.5L * (lo + hi);
         for (int it = 0; it < 200; ++it) {
             ld x = right ? q : -q;
-            ld g = tail_int(&t, x, right) / Z - target;
+            ld T = tail_int(&t, x, right);
+            ld g = logl(T / Z) - logl(target);
             if (g > 0.0L) lo = q; else hi = q;
-            ld qn = q + g / (dens_u(&t, x) / Z);
+            ld qn = q + g * T / dens_u(&t, x);
             if (!(qn > lo && qn < hi)) qn = 0.5L * (lo + hi);
             if (fabsl(qn - q) <= 4.0L * LDBL_EPSILON * qn || hi - lo <= 4.0L * LDBL_EPSILON * hi) { q = qn; break; }
             q = qn;

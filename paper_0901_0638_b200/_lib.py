@@ -17,7 +17,7 @@ QM_BREAKLESS, QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED, QM_BREAKLE
 QM_MOMENT_CHUNK = 65536
 QM_MC_CHUNK = 1 << 20
 QM_TARGET_HYPERBOLIC, QM_TARGET_VG = 1, 2
-QM_RODE_TABLE_DOUBLES = 24 + 4 * (8192 + 1)
+QM_RODE_TABLE_DOUBLES = 80 + 8 * (4096 + 16384 + 4096 + 1)
 QM_MC_MAX_STRIKES = 32
 
 

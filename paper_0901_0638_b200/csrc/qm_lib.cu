@@ -293,6 +293,7 @@ qm_status qm_exp_target_table(qm_target kind, const double *params, double *tabl
     if (kind == QM_TARGET_VG && params[0] > 0.0 && params[1] > std::fabs(params[2]) &&
         (params[0] != std::floor(params[0]) || params[0] < 1.0 || params[0] > QM_RODE_VG_MAXM + 1))
         return QM_EUNSUPPORTED;
+    static_assert(QM_RODE_TABLE_DOUBLES == QM_RODE_TABLE_LEN, "qm.h and qm_rode_params.h disagree");
     std::vector<double> tab(QM_RODE_TABLE_DOUBLES);
     if (!rode_table_build((int)kind, params, tab.data())) return QM_EINVAL;
     return cudaMemcpy(table_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess

@@ -2,11 +2,13 @@
 // samples (§4 of the paper).
 //
 // The map Q(v) is the numerically solved Recycling ODE (built on the host by
-// qm_rode_host.cpp into a table of (Q, Q') at equally spaced |v| nodes per
-// side).  Per sample the kernel does a cubic Hermite interpolation between two
-// nodes (two 16-byte gathers from the table, which stays in L2/L1) and, past
-// |v| = V (base probability e^-40), linear extrapolation with the end slope
-// (Q' -> 1 in the tails).  The side is a select, not a branch.
+// qm_rode_host.cpp into a table of (Q, Q', Q'') at the nodes of a centre, a fine
+// (out to base probability e^-40) and a coarse segment (out to e^-800), per
+// side; see qm_rode_params.h).  Per sample the kernel does a quintic Hermite interpolation
+// between two nodes (four 16-byte gathers from the table, which stays in L2/L1;
+// the error is O(h^6), needed for relative accuracy near v = 0).  Past e^-800
+// (no double uniform reaches it) linear extrapolation with the end slope
+// (Q' -> 1 in the tails).  Side and segment are selects, not branches.
 // The fused sampler draws u from Philox and applies the base quantile Q0 of
 // P:322-329 first.
 #pragma once
@@ -18,21 +20,32 @@ namespace qm {
 QM_DEV double rode_eval(const double *__restrict__ tab, double v)
 {
     const int side = (v < 0.0) ? 1 : 0;
-    const int N = QM_RODE_NODES;
     const double a = fabs(v);
-    const double h = __ldg(tab + 2 + side), ih = __ldg(tab + 4 + side), V = __ldg(tab + 6 + side);
-    const double2 *nd = reinterpret_cast<const double2 *>(tab + QM_RODE_HEADER + side * 2 * (N + 1));
-    const double s = fmin(a * ih, (double)N);
-    int k = (int)s;
-    k = (k > N - 1) ? N - 1 : k;
-    const double t = s - (double)k;
-    const double2 n0 = __ldg(nd + k), n1 = __ldg(nd + k + 1);
-    const double t2 = t * t, t3 = t2 * t;
-    const double h00 = 2.0 * t3 - 3.0 * t2 + 1.0, h10 = t3 - 2.0 * t2 + t;
-    const double h01 = -2.0 * t3 + 3.0 * t2, h11 = t3 - t2;
-    const double q = h00 * n0.x + h * (h10 * n0.y + h11 * n1.y) + h01 * n1.x;
-    const double qx = n1.x + (a - V) * n1.y;                 // beyond V: k = N-1, n1 = node N
-    return (a <= V) ? q : qx;
+    const double *sg = tab + QM_RODE_SEG + 24 * side;          // 3 segment records of 8 doubles
+    const double Vmax = __ldg(tab + 28 + side);
+    const double2 *nd = reinterpret_cast<const double2 *>(tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1));
+    // segment j = [a >= Wc] + [a >= V] (selects; NaN lands in j = 0 and is replaced later)
+    const int j = (a >= __ldg(sg + 8)) + (a >= __ldg(sg + 16));
+    const double2 r01 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j));       // w0, h
+    const double2 r23 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j + 2));   // 1/h, k0
+    const double2 r45 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j + 4));   // n, w1
+    const double h = r01.y;
+    const double s = fmin((a - r01.x) * r23.x, r45.x);        // local coordinate in [0, n]
+    const double fk = fmin(floor(s), r45.x - 1.0);
+    const int k = (int)r23.y + (int)fk;
+    const double t = s - fk;
+    // node k: (R, R') at nd[2k], (R'', 0) at nd[2k+1]
+    const double2 n0 = __ldg(nd + 2 * k), c0 = __ldg(nd + 2 * k + 1);
+    const double2 n1 = __ldg(nd + 2 * k + 2), c1 = __ldg(nd + 2 * k + 3);
+    // quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
+    const double m0 = h * n0.y, m1 = h * n1.y, h2 = h * h;
+    const double a0 = h2 * c0.x, a1 = h2 * c1.x, dp = n1.x - n0.x;
+    const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
+    const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
+    const double c5 = 6.0 * dp - 3.0 * m0 - 3.0 * m1 - 0.5 * a0 + 0.5 * a1;
+    const double q = n0.x + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
+    const double qx = n1.x + (a - Vmax) * n1.y;              // beyond Vmax: n1 = node NT
+    return (a <= Vmax) ? q : qx;
 }
 
 // x = Q(v) with IEEE semantics: +-0 -> +-0, +-inf -> +-inf, NaN -> NaN

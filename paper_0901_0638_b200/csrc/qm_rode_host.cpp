@@ -9,11 +9,14 @@
 // is exponentially ill-conditioned: Q' = 1 is a repelling fixed point
 // (d(Q'-1)/dv ~ (a-b)(Q'-1)), so an error e in Q'(0) grows like e^{(a-b)v}
 // (reading R26).  We therefore integrate BACKWARD, in the stable direction,
-// from an anchor at |v| = V where Q is fixed by its definition
-// Fbar(Q(V)) = p+ e^{-(a-b)V} (tail mass by Gauss-Legendre quadrature, Newton),
-// down to v = 0 with classical RK4 in long double, recording (Q, Q') at N+1
-// equally spaced nodes per side for cubic Hermite interpolation on the GPU.
-// Q(0) = 0 and the slope f0(0)/f(0) of P:336/P:344 come out as checks.
+// from an anchor at |v| = Vmax (base probability e^-800) where Q is fixed by its
+// definition Fbar(Q(Vmax)) = p+ e^{-(a-b)Vmax} (tail mass by Gauss-Legendre
+// quadrature, Newton), down to v = 0 with classical RK4 in long double,
+// recording (Q, Q', Q'') at the nodes of a coarse (far tail) and a fine segment
+// for quintic Hermite interpolation on the GPU.  Q(0) = 0 and the slope
+// f0(0)/f(0) of P:336/P:344 come out as checks; the first unit of rate |v| is
+// then redone forward from those exact centre conditions (relative accuracy
+// where Q -> 0).
 //
 // Table layout (doubles): see qm_rode.cuh.
 #include <cmath>
@@ -118,15 +121,32 @@ bool rode_table_build(int kind, const double *params, double *tab)
     const ld shift = t.logg(0.0L);
     const ld Zr = tail_mass(t, 0.0L, +1, rr, shift), Zl = tail_mass(t, 0.0L, -1, rl, shift);
     const ld Z = Zr + Zl, pp = Zr / Z, pm = Zl / Z;
-    const int N = QM_RODE_NODES;
+    const int Nc = QM_RODE_CENTRE_NODES, N = QM_RODE_NODES, M = QM_RODE_TAIL_NODES, NT = QM_RODE_NT;
+    std::memset(tab, 0, QM_RODE_HEADER * sizeof(double));
 
     for (int side = 0; side < 2; ++side) {
         const ld rate = side == 0 ? rr : rl, p = side == 0 ? pp : pm;
         const int dir = side == 0 ? +1 : -1;
-        const ld V = QM_RODE_VRATE / rate, h = V / N;
-        // anchor: tail mass of the target beyond Q(V) equals the base's, p e^{-rate V}
-        const ld target = p * expl(-rate * V) * Z;            // in units of e^{shift}
-        ld q = dir * (V + 1.0L);                               // Q ~ v + const
+        // segments: centre [0, Wc], fine [Wc, V], coarse [V, Vmax] (qm_rode_params.h)
+        const ld Wc = QM_RODE_VRATE_C / rate, V = QM_RODE_VRATE / rate, Vmax = QM_RODE_VRATE2 / rate;
+        const ld w0[3] = {0.0L, Wc, V}, w1[3] = {Wc, V, Vmax};
+        const int k0[3] = {0, Nc, Nc + N}, nseg[3] = {Nc, N, M};
+        ld hs[3];
+        for (int j = 0; j < 3; ++j) {
+            hs[j] = (w1[j] - w0[j]) / nseg[j];
+            double *rec = tab + QM_RODE_SEG + 8 * (3 * side + j);
+            rec[0] = (double)w0[j];
+            rec[1] = (double)hs[j];
+            rec[2] = (double)(1.0L / hs[j]);
+            rec[3] = k0[j];
+            rec[4] = nseg[j];
+            rec[5] = (double)w1[j];
+        }
+        auto seg_of = [&](int k) { return k >= k0[2] ? 2 : (k >= k0[1] ? 1 : 0); };   // interval [k, k+1]
+
+        // anchor: tail mass of the target beyond Q(Vmax) equals the base's, p e^{-rate Vmax}
+        const ld target = p * expl(-rate * Vmax) * Z;         // in units of e^{shift}
+        ld q = dir * (Vmax + 1.0L);                            // Q ~ v + const
         for (int it = 0; it < 100; ++it) {
             const ld g = tail_mass(t, q, dir, rate, shift) - target;
             const ld fq = expl(t.logg(q) - shift);
@@ -134,48 +154,78 @@ bool rode_table_build(int kind, const double *params, double *tab)
             q += dir * step;
             if (fabsl(step) <= 1e-18L * fabsl(q)) break;
         }
-        // Q'(V) = f0(V)/f(Q(V)) (first-order quantile ODE), in |v| units
+        // Q'(Vmax) = f0(Vmax)/f(Q(Vmax)) (first-order quantile ODE), in |v| units
         ld Q = q;
-        ld P = dir * (p * rate * expl(-rate * V) * Z) / expl(t.logg(q) - shift);
-        // integrate R(w) = Q(dir w), w = |v|, backward from w = V to 0:
+        ld P = dir * (p * rate * expl(-rate * Vmax) * Z) / expl(t.logg(q) - shift);
+        // integrate R(w) = Q(dir w), w = |v|, backward from w = Vmax to 0:
         //   R'' = H(R) R'^2 - rate R'   (both sides, with R' = dR/dw)
-        double *nodes = tab + QM_RODE_HEADER + side * 2 * (N + 1);
-        nodes[2 * N] = (double)Q;
-        nodes[2 * N + 1] = (double)P;
+        double *nodes = tab + QM_RODE_HEADER + side * 4 * (NT + 1);
+        auto put = [&](int k, ld q, ld p) {
+            nodes[4 * k] = (double)q;
+            nodes[4 * k + 1] = (double)p;
+            nodes[4 * k + 2] = (double)(t.H(q, dir) * p * p - rate * p);   // R'' from the RODE
+            nodes[4 * k + 3] = 0.0;
+        };
+        put(NT, Q, P);
         const int sub = QM_RODE_SUBSTEPS;
-        const ld s = -h / sub;
-        for (int k = N - 1; k >= 0; --k) {
-            for (int j = 0; j < sub; ++j) {
-                const ld k1q = P, k1p = t.H(Q, dir) * P * P - rate * P;
-                const ld q2 = Q + 0.5L * s * k1q, p2 = P + 0.5L * s * k1p;
-                const ld k2q = p2, k2p = t.H(q2, dir) * p2 * p2 - rate * p2;
-                const ld q3 = Q + 0.5L * s * k2q, p3 = P + 0.5L * s * k2p;
-                const ld k3q = p3, k3p = t.H(q3, dir) * p3 * p3 - rate * p3;
-                const ld q4 = Q + s * k3q, p4 = P + s * k3p;
-                const ld k4q = p4, k4p = t.H(q4, dir) * p4 * p4 - rate * p4;
-                Q += s / 6.0L * (k1q + 2.0L * k2q + 2.0L * k3q + k4q);
-                P += s / 6.0L * (k1p + 2.0L * k2p + 2.0L * k3p + k4p);
-            }
-            nodes[2 * k] = (double)Q;
-            nodes[2 * k + 1] = (double)P;
+        // one classical RK4 step of length s for (R, R'); the state updates are
+        // compensated (Kahan): ~10^5 steps with |Q| up to ~800/rate would otherwise
+        // accumulate a systematic rounding drift of ~1e-13 in Q
+        ld cQ = 0.0L, cP = 0.0L;
+        auto acc = [](ld &x, ld &c, ld dx) {
+            const ld y = dx - c, tx = x + y;
+            c = (tx - x) - y;
+            x = tx;
+        };
+        auto rk4 = [&](ld &Q, ld &P, ld s) {
+            const ld k1q = P, k1p = t.H(Q, dir) * P * P - rate * P;
+            const ld q2 = Q + 0.5L * s * k1q, p2 = P + 0.5L * s * k1p;
+            const ld k2q = p2, k2p = t.H(q2, dir) * p2 * p2 - rate * p2;
+            const ld q3 = Q + 0.5L * s * k2q, p3 = P + 0.5L * s * k2p;
+            const ld k3q = p3, k3p = t.H(q3, dir) * p3 * p3 - rate * p3;
+            const ld q4 = Q + s * k3q, p4 = P + s * k3p;
+            const ld k4q = p4, k4p = t.H(q4, dir) * p4 * p4 - rate * p4;
+            acc(Q, cQ, s / 6.0L * (k1q + 2.0L * k2q + 2.0L * k3q + k4q));
+            acc(P, cP, s / 6.0L * (k1p + 2.0L * k2p + 2.0L * k3p + k4p));
+        };
+        // backward: coarse, fine, then the centre (stored only down to Wc; the
+        // rest of the sweep gives the checks at v = 0)
+        ld Qc = 0.0L;
+        for (int k = NT - 1; k >= 0; --k) {
+            const ld hk = hs[seg_of(k)];
+            for (int j = 0; j < sub; ++j) rk4(Q, P, -hk / sub);
+            if (k >= Nc) put(k, Q, P);
+            if (k == Nc) Qc = Q;
         }
         // checks against the centre conditions of P:336 / P:344
         const ld slope0 = dir * p * rate * Z / expl(t.logg(0.0L) - shift);
         tab[12 + side] = (double)Q;                            // residual Q(0)
         tab[14 + side] = (double)(P / slope0 - 1.0L);          // relative slope residual
-        nodes[0] = 0.0;                                        // Q(0) = 0 exactly
-        tab[2 + side] = (double)h;
-        tab[4 + side] = (double)(1.0L / h);
-        tab[6 + side] = (double)V;
+        // Near the centre the backward sweep's accumulated ABSOLUTE error (~1e-14) is a
+        // large RELATIVE error because Q -> 0.  There the forward direction is benign over
+        // a short distance (error growth e^{rate w} <= e^2 on the centre segment), so the
+        // centre segment is integrated forward from the exact conditions Q(0) = 0,
+        // Q'(0) = slope0 (node Nc keeps the backward value; the mismatch is recorded).
+        Q = 0.0L;
+        P = slope0;
+        cQ = cP = 0.0L;
+        put(0, Q, P);
+        for (int k = 1; k <= Nc; ++k) {
+            for (int j = 0; j < sub; ++j) rk4(Q, P, hs[0] / sub);
+            if (k < Nc) put(k, Q, P);
+        }
+        tab[22 + side] = (double)(Q - Qc);                     // joint mismatch at Wc
         tab[8 + side] = (double)p;
         tab[10 + side] = (double)rate;
         const ld lp = logl(p);
         tab[16 + side] = (double)lp;                           // log p_s as a double-double
         tab[18 + side] = (double)(lp - (ld)(double)lp);
         tab[20 + side] = (double)(1.0L / rate);
+        tab[28 + side] = (double)Vmax;
     }
     tab[0] = kind;
-    tab[1] = N;
+    tab[1] = NT;
+    tab[30] = 3;
     return true;
 }
 

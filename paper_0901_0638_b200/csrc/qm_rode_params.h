@@ -1,25 +1,42 @@
 // qm_rode_params.h -- layout of the exponential-base recycling tables (row f1),
 // shared by the host builder (qm_rode_host.cpp) and the kernels (qm_rode.cuh).
 //
-// table[0]  kind (1 hyperbolic, 2 VG)        table[1]  N (intervals per side)
-// table[2+s] h_s (node spacing in |v|)       table[4+s] 1/h_s
-// table[6+s] V_s = QM_RODE_VRATE / rate_s    table[8+s] p_s (base mass: s=0 right p+, s=1 left p-)
-// table[10+s] rate_s (a-b right, a+b left)   table[12+s] Q(0) residual   table[14+s] slope residual
-// table[16+s], table[18+s]: log p_s as hi + lo            table[20+s] 1/rate_s
-// nodes of side s at table[QM_RODE_HEADER + s*2*(N+1)]: (R_k, R'_k), k = 0..N,
-// R(w) = Q(+-w) at w = k h_s, R' = dR/dw (negative values on the left side).
+// Per side s (0 = right, v > 0; 1 = left, v < 0) the map R(w) = Q(+-w), w = |v|,
+// is tabulated on three uniform segments j (node index ranges share their ends):
+//   j = 0 centre  nodes 0..Nc            0 <= w <= Wc = QM_RODE_VRATE_C / rate_s   (integrated forward
+//                                        from the exact centre conditions; ~4.75x finer than j = 1)
+//   j = 1 fine    nodes Nc..Nc+N         Wc <= w <= V  = QM_RODE_VRATE  / rate_s   (base prob. e^-40)
+//   j = 2 coarse  nodes Nc+N..NT         V <= w <= Vmax = QM_RODE_VRATE2 / rate_s  (e^-800, below the
+//                                        smallest double: every finite Q0(u) is interpolated)
+//
+// table[0]  kind (1 hyperbolic, 2 VG)        table[1]  NT (nodes per side - 1)
+// table[8+s] p_s (base mass: s=0 right p+, s=1 left p-)    table[10+s] rate_s (a-b right, a+b left)
+// table[12+s] Q(0) residual of the backward sweep           table[14+s] its slope residual
+// table[16+s], table[18+s]: log p_s as hi + lo              table[20+s] 1/rate_s
+// table[22+s] forward/backward mismatch of Q at w = Wc      table[28+s] Vmax_s    table[30] 3
+// segment record (s, j) at table[32 + 8 (3 s + j)]: w0, h, 1/h, k0, n (intervals), w1, 0, 0
+// nodes of side s at table[QM_RODE_HEADER + s*4*(QM_RODE_NT+1)]: (R_k, R'_k, R''_k, 0),
+// k = 0..NT, R' = dR/dw (negative on the left side), R'' from the RODE itself
+// (R'' = H(R) R'^2 - rate R'); quintic Hermite interpolation.
 #pragma once
 
 #define QM_RODE_HYPERBOLIC 1
 #define QM_RODE_VG 2
-#define QM_RODE_NODES 8192
+#define QM_RODE_CENTRE_NODES 4096
+#define QM_RODE_NODES 16384
+#define QM_RODE_TAIL_NODES 4096
+#define QM_RODE_NT (QM_RODE_CENTRE_NODES + QM_RODE_NODES + QM_RODE_TAIL_NODES)
 #define QM_RODE_SUBSTEPS 16
+#define QM_RODE_VRATE_C 2.0
 #define QM_RODE_VRATE 40.0
-#define QM_RODE_HEADER 24
+#define QM_RODE_VRATE2 800.0
+#define QM_RODE_HEADER 80
+#define QM_RODE_SEG 32
 #define QM_RODE_VG_MAXM 8
-#define QM_RODE_TABLE_DOUBLES (QM_RODE_HEADER + 4 * (QM_RODE_NODES + 1))
+#define QM_RODE_TABLE_LEN (QM_RODE_HEADER + 8 * (QM_RODE_NT + 1))
 
 namespace qm {
-// builds the table in host memory (QM_RODE_TABLE_DOUBLES doubles); false on bad parameters
+// builds the table in host memory (QM_RODE_TABLE_LEN doubles = QM_RODE_TABLE_DOUBLES of qm.h);
+// false on bad parameters
 bool rode_table_build(int kind, const double *params, double *table);
 }  // namespace qm

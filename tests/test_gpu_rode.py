@@ -1,7 +1,7 @@
 """GPU parity of the exponential-base recycling into hyperbolic / VG samples
-(SURVEY §8 row f1): the kernel (cubic Hermite on the RODE table) against the
-oracle's exact map Q(v) = F^-1(F0(v)).  Bar: the method's accuracy, 2e-11
-relative in fp64 (table 1e-12 + interpolation), and 2 ulp + that in fp32."""
+(SURVEY §8 row f1): the kernel (quintic Hermite on the RODE table) against the
+oracle's exact map Q(v) = F^-1(F0(v)).  Bar: 1e-14 relative in fp64 (table ~1e-16
++ quintic interpolation on a segment grid ~3e-16; measured by emulation), 2 ulp in fp32."""
 import numpy as np
 import pytest
 import torch
@@ -29,15 +29,18 @@ def _base_samples(kind, par, n, seed=5):
 @pytest.mark.parametrize("kind,par", CASES)
 def test_recycle_exp_to_target_vs_exact_map(kind, par):
     tab = Q.qm_exp_target_table(kind, par)
-    v = np.concatenate([_base_samples(kind, par, 400), [0.0, -0.0, 1e-12, -1e-9, 60.0, -70.0]])
+    a, b = (par[0], par[1]) if kind == O.HYPERBOLIC else (par[1], par[2])
+    rr, rl = a - b, a + b
+    # base samples, the centre, both segment joints (base probability e^-40) and the
+    # far tail out to e^-740 (the smallest double uniform gives e^-744)
+    far = [1e-12, -1e-9, 40 / rr, -40 / rl, 40 / rr * (1 + 1e-9), 60.0, -70.0, 300 / rr, -500 / rl, 740 / rr, -740 / rl]
+    v = np.concatenate([_base_samples(kind, par, 400), [0.0, -0.0], far])
     fn = Q.qm_recycle_exp_to_hyperbolic if kind == O.HYPERBOLIC else Q.qm_recycle_exp_to_vg
     g = fn(torch.from_numpy(v).cuda(), tab).cpu().numpy()
     ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
     nz = v != 0
     rel = np.abs(g[nz] / ex[nz] - 1)
-    inside = np.abs(v[nz]) < 35.0
-    assert rel[inside].max() < 2e-11, rel.max()
-    assert rel.max() < 1e-7                       # linear extrapolation beyond base probability e^-40
+    assert rel.max() < 1e-14, (rel.max(), v[nz][np.argmax(rel)])
     assert g[~nz].tolist() == v[~nz].tolist() and np.array_equal(np.signbit(g[~nz]), np.signbit(v[~nz]))
     g32 = fn(torch.from_numpy(v.astype(np.float32)).cuda(), tab).cpu().numpy()
     ex32 = O.recycle_exp_to_target(kind, par, v.astype(np.float32).astype(np.float64))
@@ -74,7 +77,10 @@ def test_base_quantile_and_moments():
     v = Q.qm_exp_base_quantile(torch.from_numpy(u).cuda(), tab).cpu().numpy()
     ul = u.astype(np.longdouble)
     ref = np.where(u < float(pm), np.log(ul / pm) / 1.0, -np.log((1 - ul) / pp) / 3.0)
-    assert np.max(np.abs(v - ref.astype(np.float64)) / np.maximum(1e-300, np.abs(ref.astype(np.float64)))) < 1e-13
+    # the kernel adds log p (p in long double) while ref divides by p rounded to double:
+    # |d log p| <= 1.1e-16, so near v = 0 only an absolute bar of that size is meaningful
+    err = np.abs(v - ref.astype(np.float64))
+    assert np.all(err <= 1e-15 * np.abs(ref.astype(np.float64)) + 2e-16), err.max()
     x = Q.qm_exp_target_philox(1 << 24, tab, 11, 0)
     mp.mp.dps = 20
     f = lambda t: mp.exp(-2.0 * mp.sqrt(0.25 + t * t) - 1.0 * t)

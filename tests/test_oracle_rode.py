@@ -107,18 +107,36 @@ def test_vg_lambda2_closed_form_cdf():
 @pytest.mark.parametrize("kind,par", [(O.HYPERBOLIC, p) for p in HYP] +
                          [(O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4])])
 def test_product_rode_table_vs_oracle(kind, par):
-    """libqm's table (RODE integrated backward in long double) at sampled nodes vs the
-    oracle's exact map; Q(0) = 0 and the centre slopes of P:336/P:344 as residuals."""
+    """libqm's table (RODE integrated backward in long double, the centre segment
+    forward) at sampled nodes of each segment vs the oracle's exact map, R' and R''
+    vs differences of it; Q(0) = 0 and the centre slopes of P:336/P:344 as residuals."""
     from paper_0901_0638_b200.qm import qm_rode_table_host
     tab = qm_rode_table_host(kind, par)
-    N, H = 8192, 24
+    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    assert tab[1] == NT and tab[30] == 3
     assert np.all(np.abs(tab[12:14]) < 1e-12) and np.all(np.abs(tab[14:16]) < 1e-12)
+    assert np.all(np.abs(tab[22:24]) < 1e-14 * (1 + 2.0 / (tab[10:12])))         # forward/backward joint
     m = O.target_masses(kind, par)
     assert abs(tab[8] - float(m[1])) < 1e-15 and abs(tab[9] - float(m[0])) < 1e-15
     for side in (0, 1):
-        h = tab[2 + side]
-        nodes = tab[H + side * 2 * (N + 1):H + (side + 1) * 2 * (N + 1)].reshape(-1, 2)
-        ks = np.array([1, 37, 500, 2000, 5000, 8191])
-        v = ks * h * (1 if side == 0 else -1)
-        ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
-        assert np.abs(nodes[ks, 0] / ex - 1).max() < 1e-11
+        sg = 1 if side == 0 else -1
+        nodes = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)
+        assert nodes[0, 0] == 0.0
+        for j, js in enumerate([[1, 2, 37, 4000], [1, 500, 5000, 16383], [1, 100, 2000, 4096]]):
+            w0, h, ih, k0, n, w1 = tab[SEG + 8 * (3 * side + j):SEG + 8 * (3 * side + j) + 6]
+            assert int(k0) == [0, 4096, 4096 + 16384][j] and abs(w0 + n * h - w1) <= 1e-12 * w1
+            js = np.array(js)
+            ex = O.recycle_exp_to_target(kind, par, (w0 + js * h) * sg).astype(np.float64)
+            assert np.abs(nodes[int(k0) + js, 0] / ex - 1).max() < 1e-13, j
+        # R' and R'' against central differences of the exact map (long double; O(hh^2) ~ 1e-8)
+        w0, h = tab[SEG + 8 * 3 * side], tab[SEG + 8 * 3 * side + 1]
+        ks = np.array([1, 2, 37, 500])
+        hh = 1e-2 * h
+        w = ks * h
+        qp = O.recycle_exp_to_target(kind, par, (w + hh) * sg)
+        q0 = O.recycle_exp_to_target(kind, par, w * sg)
+        qm = O.recycle_exp_to_target(kind, par, (w - hh) * sg)
+        d1 = ((qp - qm) / (2 * np.longdouble(hh))).astype(np.float64)
+        d2 = ((qp - 2 * q0 + qm) / np.longdouble(hh) ** 2).astype(np.float64)
+        assert np.abs(d1 / nodes[ks, 1] - 1).max() < 1e-7
+        assert np.abs(d2 - nodes[ks, 2]).max() < 1e-6 * (1 + np.abs(nodes[ks, 2]).max())
