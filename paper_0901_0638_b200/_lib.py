@@ -6,10 +6,12 @@ import fails loudly, and every entry point checks its status code.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libqm.so"
+# QM_LIB_PATH: load another build of the same sources (A/B experiments only)
+LIB_PATH = Path(os.environ.get("QM_LIB_PATH", str(_HERE / "libqm.so")))
 
 QM_OK, QM_EINVAL, QM_EUNSUPPORTED, QM_ECUDA = 0, 1, 2, 3
 QM_F32, QM_F64 = 1, 2

@@ -29,9 +29,11 @@ def up_to_date() -> bool:
     return all(s.stat().st_mtime <= t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: Path = None, defines=()) -> Path:
+    """`out`/`defines`: an A/B build of the same sources (experiments only)."""
+    if out is None and not force and up_to_date():
         return LIB
+    lib = LIB if out is None else Path(out)
     # host-side parameter setup (C++, long double / __float128)
     objs = []
     for src in sorted(CSRC.glob("*.cpp")):
@@ -41,13 +43,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-I", str(ROOT / "include"), str(CSRC / "qm_lib.cu"), *map(str, objs), "-lquadmath",
-           "-o", str(LIB)]
+           *[f"-D{d}" for d in defines], "-o", str(lib)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
     for o in objs:
         o.unlink(missing_ok=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

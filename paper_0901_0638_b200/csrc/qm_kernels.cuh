@@ -90,6 +90,98 @@ using TmaCfgE = TmaCfg<12, 4, 6144, 2>;      // 2 CTAs/SM, 24 consumer warps, 2 
 using TmaCfgH = TmaCfg<12, 2, 6144, 3>;      // 3 CTAs/SM, 36 consumer warps, 3 x 48 KB
 using TmaCfgI = TmaCfg<8, 3, 4096, 4>;       // 4 CTAs/SM, 32 consumer warps, 4 x 48 KB
 
+// one float4 of u -> one float4 of z: a single vote per warp picks the fast path
+// (no special-value code) or the careful path for all 4 x 32 samples
+template <int ALG>
+QM_DEV float4 normal4_f32(const float4 a)
+{
+    const float x[4] = {a.x, a.y, a.z, a.w};
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= fast_vv_min_f32<ALG>());
+    float y[4];
+    if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+        for (int k = 0; k < 4; k += 2) {
+            const float oa = __fsub_rn(1.0f, x[k]), ob = __fsub_rn(1.0f, x[k + 1]);
+            const float2 lz = neg_log2x_f32x2(fminf(x[k], oa), fminf(x[k + 1], ob));
+            y[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.x), x[k], oa);
+            y[k + 1] = apply_sign_f32(rat32<fast_alg<ALG>()>(lz.y), x[k + 1], ob);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
+    }
+    return make_float4(y[0], y[1], y[2], y[3]);
+}
+
+// G float4 (4G samples) per lane under ONE vote: the fast path of all 4G samples
+// is one basic block, so the scheduler can interleave their log chains (FFMA2)
+// and rational chains (DFMA) -- the fp32 log alone is a 9-deep dependent chain.
+template <int ALG, int G>
+QM_DEV void normal_group_f32(float4 *a)
+{
+    constexpr int NS = 4 * G;
+    float x[NS];
+#pragma unroll
+    for (int j = 0; j < G; ++j) { x[4 * j] = a[j].x; x[4 * j + 1] = a[j].y; x[4 * j + 2] = a[j].z; x[4 * j + 3] = a[j].w; }
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= fast_vv_min_f32<ALG>());
+    float y[NS];
+    if (__all_sync(0xffffffffu, ok)) {
+        float om[NS], zl[NS];
+#pragma unroll
+        for (int k = 0; k < NS; k += 2) {
+            om[k] = __fsub_rn(1.0f, x[k]);
+            om[k + 1] = __fsub_rn(1.0f, x[k + 1]);
+            const float2 lz = neg_log2x_f32x2(fminf(x[k], om[k]), fminf(x[k + 1], om[k + 1]));
+            zl[k] = lz.x; zl[k + 1] = lz.y;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) y[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(zl[k]), x[k], om[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) a[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+}
+
+template <int ALG, int G>
+struct MapNormalF32 {
+    template <int PER>
+    QM_DEV void map_slice(float4 *a) const
+    {
+        static_assert(PER % G == 0, "group size must divide the per-lane vector count");
+#pragma unroll
+        for (int j = 0; j < PER; j += G) normal_group_f32<ALG, G>(a + j);
+    }
+};
+
+// TMA-in / STG-out shapes (tma_load_map): NC consumer warps, STAGES x TILE
+// floats of shared memory per CTA, MINB CTAs per SM
+template <int NC_, int STAGES_, int TILE_, int MINB_, int G_ = 1>
+struct TlCfg {
+    static constexpr int NC = NC_, STAGES = STAGES_, TILE = TILE_, MINB = MINB_, THREADS = 32 * (NC_ + 1);
+    static constexpr int UNROLL = 1, G = G_;
+    static_assert(TILE_ % (4 * 32 * NC_) == 0, "tile must split evenly over the consumer warps");
+};
+using TlCfgJ = TlCfg<16, 4, 8192, 1>;       // 1 CTA/SM, 16 consumer warps, 4 x 32 KB
+using TlCfgK = TlCfg<16, 3, 8192, 2>;       // 2 CTAs/SM, 2 x 3 x 32 KB
+using TlCfgL = TlCfg<16, 4, 8192, 1, 2>;    // J, 2 float4 per vote
+using TlCfgM = TlCfg<24, 4, 12288, 1, 2>;   // 1 CTA/SM, 24 consumer warps, 4 x 48 KB, 2 float4 per vote
+using TlCfgN = TlCfg<12, 4, 6144, 2, 2>;    // 2 CTAs/SM, 2 x 12 consumer warps, 2 x 4 x 24 KB, 2 float4 per vote
+
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
+k_normal_f32_tl(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
+{
+    tma_load_map<float4, CFG::TILE / 4, CFG::STAGES, CFG::NC>(reinterpret_cast<const float4 *>(u),
+                                                             reinterpret_cast<float4 *>(z), ntiles,
+                                                             MapNormalF32<ALG, CFG::G>{});
+}
+
 template <int ALG, class CFG>
 struct OpNormalF32 {
     QM_DEV void tile(float *t, int ctid, int nct) const
@@ -250,32 +342,35 @@ k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned
     const int64_t nchunks = (nb + 32 * V - 1) / (32 * V);
     for (int64_t c = gwarp; c < nchunks; c += nwarps) {
         const int64_t base = c * (32 * V) + lane;
+        // all V blocks (4V samples) in one basic block, stores after the math, so
+        // the scheduler can interleave the Philox rounds, logs and rationals
+        float r[4 * V];
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-            const int64_t b = base + 32 * j;
-            const uint4 w = philox_block(c0 + (unsigned long long)b, seed);
-            float r[4];
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-            if (MODE == 0) {
+            const uint4 w = philox_block(c0 + (unsigned long long)(base + 32 * j), seed);
+            r[4 * j] = u01_f32(w.x); r[4 * j + 1] = u01_f32(w.y);
+            r[4 * j + 2] = u01_f32(w.z); r[4 * j + 3] = u01_f32(w.w);
+        }
+        if (MODE == 1) {
+            float om[4 * V], zl[4 * V];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) r[k] = u01_f32(ws[k]);
-            } else {
-                float uu[4], om[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) { uu[k] = u01_f32(ws[k]); om[k] = __fsub_rn(1.0f, uu[k]); }
-                const float2 l01 = neg_log2x_f32x2(fminf(uu[0], om[0]), fminf(uu[1], om[1]));
-                const float2 l23 = neg_log2x_f32x2(fminf(uu[2], om[2]), fminf(uu[3], om[3]));
-                r[0] = apply_sign_f32(rat32<fast_alg<ALG>()>(l01.x), uu[0], om[0]);
-                r[1] = apply_sign_f32(rat32<fast_alg<ALG>()>(l01.y), uu[1], om[1]);
-                r[2] = apply_sign_f32(rat32<fast_alg<ALG>()>(l23.x), uu[2], om[2]);
-                r[3] = apply_sign_f32(rat32<fast_alg<ALG>()>(l23.y), uu[3], om[3]);
+            for (int k = 0; k < 4 * V; k += 2) {
+                om[k] = __fsub_rn(1.0f, r[k]);
+                om[k + 1] = __fsub_rn(1.0f, r[k + 1]);
+                const float2 l = neg_log2x_f32x2(fminf(r[k], om[k]), fminf(r[k + 1], om[k + 1]));
+                zl[k] = l.x; zl[k + 1] = l.y;
             }
-            const int64_t i = 4 * b;
+#pragma unroll
+            for (int k = 0; k < 4 * V; ++k) r[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(zl[k]), r[k], om[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = 4 * (base + 32 * j);
             if (vec && i + 3 < n) {
-                st_stream_f4(reinterpret_cast<float4 *>(z + i), make_float4(r[0], r[1], r[2], r[3]));
+                st_stream_f4(reinterpret_cast<float4 *>(z + i), make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) if (i + k < n) z[i + k] = r[k];
+                for (int k = 0; k < 4; ++k) if (i + k < n) z[i + k] = r[4 * j + k];
             }
         }
     }
@@ -437,6 +532,27 @@ struct OpExp2nF32 {
         }
     }
 };
+
+template <int ALG>
+struct MapExp2nF32 {
+    template <int PER>
+    QM_DEV void map_slice(float4 *a) const
+    {
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            a[j] = make_float4(exp2n_f32<ALG>(a[j].x), exp2n_f32<ALG>(a[j].y), exp2n_f32<ALG>(a[j].z),
+                               exp2n_f32<ALG>(a[j].w));
+    }
+};
+
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
+k_exp2n_f32_tl(const float *__restrict__ v, float *__restrict__ z, int64_t ntiles)
+{
+    tma_load_map<float4, CFG::TILE / 4, CFG::STAGES, CFG::NC>(reinterpret_cast<const float4 *>(v),
+                                                             reinterpret_cast<float4 *>(z), ntiles,
+                                                             MapExp2nF32<ALG>{});
+}
 
 template <int ALG, class CFG>
 __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)

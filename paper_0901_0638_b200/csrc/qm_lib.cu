@@ -49,6 +49,17 @@ int grid_for(int64_t work_items, int items_per_block, int per_sm)
     return (int)(g < 1 ? 1 : g);
 }
 
+// persistent grid: as many blocks as can be resident at once (one wave), but
+// never more than the work needs
+template <typename K>
+int grid_resident(K kernel, int threads, int64_t work_items, int items_per_block)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return grid_for(work_items, items_per_block, per_sm);
+}
+
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 qm_status launched()
@@ -58,16 +69,19 @@ qm_status launched()
 
 bool bad_ptrs(const void *a, const void *b, int64_t n) { return n > 0 && (a == nullptr || b == nullptr); }
 
-// QM_STREAM_PATH=ldg forces the register-pipelined LDG kernels (A/B diagnostics)
-bool tma_enabled()
+// QM_STREAM_PATH (A/B diagnostics): "ldg" forces the register-pipelined LDG
+// kernels, "tma" the in-place TMA load/store pipeline; default "tl" (TMA in,
+// streaming stores out)
+int stream_path()
 {
-    static int on = -1;
-    if (on < 0) {
+    static int p = -1;
+    if (p < 0) {
         const char *e = getenv("QM_STREAM_PATH");
-        on = (e && strcmp(e, "ldg") == 0) ? 0 : 1;
+        p = (e && strcmp(e, "ldg") == 0) ? 0 : (e && strcmp(e, "tma") == 0) ? 1 : 2;
     }
-    return on == 1;
+    return p;
 }
+bool tma_enabled() { return stream_path() != 0; }
 
 // fp32 elementwise map: whole tiles through the TMA pipeline (persistent CTAs),
 // the remainder (< 1 tile) and misaligned arrays through the LDG kernel.
@@ -104,9 +118,29 @@ char tma_cfg()
     return c;
 }
 
+// QM_TL_CFG=J..N selects the TMA-in/STG-out shape (default L)
+char tl_cfg()
+{
+    static char c = 0;
+    if (!c) {
+        const char *e = getenv("QM_TL_CFG");
+        c = (e && e[0] >= 'J' && e[0] <= 'N') ? e[0] : 'L';
+    }
+    return c;
+}
+
 template <int ALG>
 qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
 {
+    if (stream_path() == 2) {
+        switch (tl_cfg()) {
+        case 'K': return launch_stream_f32<TlCfgK>(k_normal_f32_tl<ALG, TlCfgK>, k_normal_f32<ALG>, u, z, n, s);
+        case 'L': return launch_stream_f32<TlCfgL>(k_normal_f32_tl<ALG, TlCfgL>, k_normal_f32<ALG>, u, z, n, s);
+        case 'M': return launch_stream_f32<TlCfgM>(k_normal_f32_tl<ALG, TlCfgM>, k_normal_f32<ALG>, u, z, n, s);
+        case 'N': return launch_stream_f32<TlCfgN>(k_normal_f32_tl<ALG, TlCfgN>, k_normal_f32<ALG>, u, z, n, s);
+        default: return launch_stream_f32<TlCfgJ>(k_normal_f32_tl<ALG, TlCfgJ>, k_normal_f32<ALG>, u, z, n, s);
+        }
+    }
     switch (tma_cfg()) {
     case 'A': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
     case 'C': return launch_stream_f32<TmaCfgC>(k_normal_f32_tma<ALG, TmaCfgC>, k_normal_f32<ALG>, u, z, n, s);
@@ -123,6 +157,8 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
 template <int ALG>
 qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
 {
+    if (stream_path() == 2)
+        return launch_stream_f32<TlCfgJ>(k_exp2n_f32_tl<ALG, TlCfgJ>, k_exp2n_f32<ALG>, v, z, n, s);
     return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
 }
 
@@ -219,10 +255,17 @@ static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_
     // plain rational there, so QM_BREAKLESS_TAIL runs the QM_BREAKLESS kernel
     if (alg == QM_BREAKLESS_TAIL) alg = QM_BREAKLESS;
     if (p == QM_F32) {
-        const int g = grid_for((n + 3) / 4, kThreads * 2, 8);
-        if (mode == 0) k_philox_f32<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
-        else if (alg == QM_BREAKLESS) k_philox_f32<1, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
-        else k_philox_f32<1, ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        const int64_t nb = (n + 3) / 4;
+        if (mode == 0) {
+            auto k = k_philox_f32<0, ALG_BREAKLESS>;
+            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        } else if (alg == QM_BREAKLESS) {
+            auto k = k_philox_f32<1, ALG_BREAKLESS>;
+            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        } else {
+            auto k = k_philox_f32<1, ALG_BREAKLESS77>;
+            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+        }
     } else {
         const int g = grid_for((n + 1) / 2, kThreads, 8);
         if (mode == 0) k_philox_f64<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);

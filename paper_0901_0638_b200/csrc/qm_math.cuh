@@ -71,19 +71,20 @@ __constant__ double kD13Q[14] = {
     0.0040618506206078995821, 0.00014919732843986856251, 2.7477061392049947066e-6,
     2.2815008011613816939e-8, 7.0445790305953963457e-11, 5.1535907808963289678e-14};
 
-// fp32 log: log1p(f) = f + f^2 R(f), f in [-1/3, 1/3); R: Chebyshev fit
-// (tools/fit_log.py), |error of R| < 3.2e-8 -> < 0.2 ulp of log1p.
-#define QM_LR0 -0.5f
-#define QM_LR1 0.33333271741867065f
-#define QM_LR2 -0.24999944865703583f
-#define QM_LR3 0.20007233321666718f
-#define QM_LR4 -0.16673316061496735f
-#define QM_LR5 0.140558123588562f
-#define QM_LR6 -0.12288721650838852f
-#define QM_LR7 0.13748309016227722f
-#define QM_LR8 -0.12422200292348862f
-#define QM_LN2F_HI 0.693145751953125f        // 16 significant bits: e*hi exact for |e| < 256
-#define QM_LN2F_LO 1.428606765330187e-06f
+// fp32 log: log1p(f) = f + f^2 R(f), f in [-1/3, 1/3); R: degree-7 Chebyshev fit
+// (tools/fit_log.py), |error of R| < 2.1e-7.  Where the log's relative error
+// reaches z unscaled (e = 0, f -> -1/3) it is < 0.3 ulp of z; the fp32 map stays
+// <= 1.67 ulp over the whole fp32 grid (degree 8 and a two-part ln2: 1.42 ulp,
+// one FFMA2 per sample pair more for each).
+#define QM_LR0 -0.49999985098838806f
+#define QM_LR1 0.33333319425582886f
+#define QM_LR2 -0.2500414550304413f
+#define QM_LR3 0.20003780722618103f
+#define QM_LR4 -0.16483017802238464f
+#define QM_LR5 0.14118309319019318f
+#define QM_LR6 -0.15040764212608337f
+#define QM_LR7 0.1342574954032898f
+#define QM_LN2F 0.6931471824645996f          // (float)ln 2
 
 // fp64 log: log1p(f) = 2 atanh(s) = 2s + s^3 T(s^2), s = f/(2+f) in [-0.2, 1/7];
 // T: Chebyshev fit on w in [0, 1/25], relative error < 4e-17 (term is < 1.3% of 2s)
@@ -94,6 +95,17 @@ __constant__ double kLogT[8] = {0.6666666666666666, 0.400000000000078, 0.2857142
 #define QM_LN2_LO 1.90821492927058770002e-10
 
 // ------------------------------------------------------------- fp32 pieces
+#define QM_LOG_R(r, f, FMA, C)                                                      \
+    r = FMA(C(QM_LR7), f, C(QM_LR6));                                               \
+    r = FMA(r, f, C(QM_LR5));                                                       \
+    r = FMA(r, f, C(QM_LR4));                                                       \
+    r = FMA(r, f, C(QM_LR3));                                                       \
+    r = FMA(r, f, C(QM_LR2));                                                       \
+    r = FMA(r, f, C(QM_LR1));                                                       \
+    r = FMA(r, f, C(QM_LR0));
+#define QM_C1(x) (x)
+#define QM_C2(x) make_float2((x), (x))
+
 // z = -log(2 vv) for vv a normal float in (0, 1/2]; `eadj` adds to the binary
 // exponent (used to pre-scale subnormals by 2^24).  <= ~1 ulp.
 QM_DEV float neg_log2x_f32(float vv, int eadj)
@@ -102,20 +114,13 @@ QM_DEV float neg_log2x_f32(float vv, int eadj)
     const int32_t e = (k >> 23) + 1 + eadj;                             // +1: the factor 2
     const float m = __uint_as_float(((uint32_t)k & 0x7fffffu) + 0x3f2aaaabu);   // [2/3, 4/3)
     const float f = __fsub_rn(m, 1.0f);                                 // exact (Sterbenz)
-    float r = __fmaf_rn(QM_LR8, f, QM_LR7);
-    r = __fmaf_rn(r, f, QM_LR6);
-    r = __fmaf_rn(r, f, QM_LR5);
-    r = __fmaf_rn(r, f, QM_LR4);
-    r = __fmaf_rn(r, f, QM_LR3);
-    r = __fmaf_rn(r, f, QM_LR2);
-    r = __fmaf_rn(r, f, QM_LR1);
-    r = __fmaf_rn(r, f, QM_LR0);
+    float r;
+    QM_LOG_R(r, f, __fmaf_rn, QM_C1)
     const float f2 = __fmul_rn(f, f);
     const float L = __fmaf_rn(f2, r, f);                                // log1p(f)
     // (float)e without I2F: 1.5*2^23 + e as bits, minus 1.5*2^23 (|e| < 2^22)
     const float ef = __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
-    float zf = __fmaf_rn(ef, QM_LN2F_HI, L);
-    zf = __fmaf_rn(ef, QM_LN2F_LO, zf);
+    const float zf = __fmaf_rn(ef, QM_LN2F, L);
     return -zf;
 }
 
@@ -128,21 +133,14 @@ QM_DEV float2 neg_log2x_f32x2(float vva, float vvb, int eadj = 0)
     const float2 m = make_float2(__uint_as_float(((uint32_t)ka & 0x7fffffu) + 0x3f2aaaabu),
                                  __uint_as_float(((uint32_t)kb & 0x7fffffu) + 0x3f2aaaabu));
     const float2 f = add2(m, make_float2(-1.0f, -1.0f));
-    float2 r = fma2(make_float2(QM_LR8, QM_LR8), f, make_float2(QM_LR7, QM_LR7));
-    r = fma2(r, f, make_float2(QM_LR6, QM_LR6));
-    r = fma2(r, f, make_float2(QM_LR5, QM_LR5));
-    r = fma2(r, f, make_float2(QM_LR4, QM_LR4));
-    r = fma2(r, f, make_float2(QM_LR3, QM_LR3));
-    r = fma2(r, f, make_float2(QM_LR2, QM_LR2));
-    r = fma2(r, f, make_float2(QM_LR1, QM_LR1));
-    r = fma2(r, f, make_float2(QM_LR0, QM_LR0));
+    float2 r;
+    QM_LOG_R(r, f, fma2, QM_C2)
     const float2 f2 = mul2(f, f);
     const float2 L = fma2(f2, r, f);
     const float2 ef = add2(make_float2(__int_as_float(0x4B400000 + (ka >> 23) + 1 + eadj),
                                        __int_as_float(0x4B400000 + (kb >> 23) + 1 + eadj)),
                            make_float2(-12582912.0f, -12582912.0f));
-    float2 zf = fma2(ef, make_float2(QM_LN2F_HI, QM_LN2F_HI), L);
-    zf = fma2(ef, make_float2(QM_LN2F_LO, QM_LN2F_LO), zf);
+    const float2 zf = fma2(ef, make_float2(QM_LN2F, QM_LN2F), L);
     return make_float2(-zf.x, -zf.y);
 }
 

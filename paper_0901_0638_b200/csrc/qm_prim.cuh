@@ -44,6 +44,9 @@ QM_DEV void st_stream_d2(double2 *p, double2 v)
     asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+QM_DEV void st_stream(float4 *p, float4 v) { st_stream_f4(p, v); }
+QM_DEV void st_stream(double2 *p, double2 v) { st_stream_d2(p, v); }
+
 // Packed fp32 pair arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): two
 // independent IEEE round-to-nearest operations per instruction.
 QM_DEV float2 fma2(float2 a, float2 b, float2 c)

@@ -124,3 +124,75 @@ __device__ __forceinline__ void tma_stream_map(const T *__restrict__ in, T *__re
 }
 
 }  // namespace qm
+
+namespace qm {
+
+// ----------------------------------------------------------------------------
+// TMA-in / STG-out pipeline ("load map").  Same producer as tma_stream_map, but
+// the consumers do not write the tile back into shared memory:
+//
+//   * each consumer warp owns a contiguous 1/NC slice of a tile; it waits on
+//     "full", reads its slice into registers (LDS.128, PER vectors per lane),
+//     and its lane 0 arrives on "empty" (count NC) at once -- the stage goes
+//     back to the producer before the math, not after the tile's store;
+//   * the warp then maps its registers and writes them with 128-bit streaming
+//     stores (st.global.cs) straight to global memory: stores need no
+//     completion, so nothing of the output is held in shared memory;
+//   * no CTA-wide barrier per tile: a warp that finishes its slice goes on to
+//     the next tile without waiting for the other warps.
+//
+// OP::map_slice<PER>(V a[PER]) maps a lane's PER 16-byte vectors in place.
+template <typename V, int TILE_VECS, int STAGES, int NC, typename OP>
+__device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__restrict__ out, int64_t ntiles, OP op)
+{
+    static_assert(sizeof(V) == 16, "16-byte vectors");
+    static_assert(TILE_VECS % (32 * NC) == 0, "tile must split evenly over the consumer warps");
+    constexpr int PER = TILE_VECS / (32 * NC);
+    constexpr uint32_t TILE_BYTES = TILE_VECS * 16;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V *tiles = reinterpret_cast<V *>(smem_raw);
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int64_t first = blockIdx.x, step = gridDim.x;
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int64_t k = 0;
+            for (int64_t t = first; t < ntiles; t += step, ++k) {
+                if (k >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&full[s], TILE_BYTES);
+                bulk_g2s(tiles + (size_t)s * TILE_VECS, in + t * TILE_VECS, TILE_BYTES, &full[s]);
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+        return;
+    }
+    const int w = warp - 1;
+    const int off = w * (PER * 32) + lane;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = first; t < ntiles; t += step) {
+        mbar_wait(&full[s], ph);
+        const V *tile = tiles + (size_t)s * TILE_VECS + off;
+        V a[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) a[j] = tile[32 * j];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        op.template map_slice<PER>(a);
+        V *o = out + t * TILE_VECS + off;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) st_stream(o + 32 * j, a[j]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+}
+
+}  // namespace qm
