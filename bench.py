@@ -113,13 +113,15 @@ def dist_setup(gpus):
 
 
 # ------------------------------------------------------------ reference arm
-def oracle_rate(n_sample, threads, seed=SEED, chunk=1 << 22):
+def oracle_rate(n_sample, threads, seed=SEED, chunk=None):
     """Time the oracle (same formula, long double) over a bounded sample on host
     cores: `threads` workers map chunks of the sample (ctypes releases the GIL)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import oracle as O
     from synth import inputs as I
+    if chunk is None:                    # every worker gets work, chunks of <= 4 Mi samples
+        chunk = max(1 << 14, min(1 << 22, -(-n_sample // (4 * threads))))
     u = I.uniform_grid(n_sample, seed, np.float32)
     bounds = [(i, min(i + chunk, n_sample)) for i in range(0, n_sample, chunk)]
     O.lib()
@@ -141,7 +143,7 @@ def run_reference(args):
     import oracle as O
     O.build()
     threads = os.cpu_count() or 1
-    n_step = 1 << 20                     # bounded sample per step
+    n_step = 1 << 22                     # bounded sample per step (~15-40 ms on 16 threads)
     for _ in range(args.warmup):
         oracle_rate(n_step, threads)
     ts = []
@@ -196,11 +198,24 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     out = {}
     hbm = peaks["hbm_gbs"]
 
-    def rec(name, fn, n, bytes_per, extra=None):
+    facts = load_traffic()
+    # issue-slot ceiling: 148 SMs x 4 schedulers x 1 warp-instruction / clock
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    issue_peak = sms * 4 * peaks["sm_max_mhz"] / 1e3          # G warp-instructions / s
+
+    def rec(name, fn, n, bytes_per, extra=None, fact=None):
         ms = time_steps(fn, steps, warmup) / steps
         r = {"gsamples_s": n / (ms / 1e3) / 1e9, "ms": ms, "n": n,
              "hbm_gbs": (bytes_per * n / (ms / 1e3) / 1e9) if bytes_per else 0.0}
         r["hbm_frac"] = r["hbm_gbs"] / hbm
+        f = facts.get(fact) if fact else None
+        if f and f.get("warp_inst_per_elem"):
+            # compute-bound rows: warp-instructions per sample (ncu) x samples/s
+            # against the issue ceiling (bench measures the rate, ncu the count)
+            ach = f["warp_inst_per_elem"] * r["gsamples_s"]
+            r["roofline"] = {"bound": "issue", "achieved": ach, "peak": issue_peak,
+                             "unit": "G warp-inst/s", "frac": ach / issue_peak,
+                             "warp_inst_per_sample": f["warp_inst_per_elem"], "source": f.get("source")}
         if extra:
             r.update(extra)
         out[name] = r
@@ -209,20 +224,21 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     u64 = torch.empty(n, dtype=torch.float64, device="cuda")
     Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64, out=u64)
     z64 = torch.empty_like(u64)
-    rec("stream_f64_D13_2^28", lambda: Q.qm_normal_quantile(u64, out=z64), n, 16)
+    rec("stream_f64_D13_2^28", lambda: Q.qm_normal_quantile(u64, out=z64), n, 16, fact="stream_f64")
     zf = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
-    rec("philox_fused_f32_2^32", lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=zf), 1 << 32, 4)
+    rec("philox_fused_f32_2^32", lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=zf), 1 << 32, 4, fact="fused_f32")
     del zf
     zd = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
     rec("philox_fused_f64_2^31", lambda: Q.qm_normal_philox(1 << 31, SEED, 0, dtype=torch.float64, out=zd),
-        1 << 31, 8)
+        1 << 31, 8, fact="fused_f64")
     del zd
     # config 4: Student-t recycling of 2^30 fp64 normals (untimed producer: the fused kernel)
     zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
     tt = torch.empty_like(zn)
     for nu, K, zs in [(4.0, 10, 3.93473), (3.0, 16, 3.5667), (5.0, 16, 4.6506), (10.0, 16, 6.9584)]:
         rec(f"student_f64_nu{int(nu)}_K{K}_2^30",
-            lambda nu=nu, K=K, zs=zs: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=tt), 1 << 30, 16)
+            lambda nu=nu, K=K, zs=zs: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=tt), 1 << 30, 16,
+            fact="student" if nu == 4.0 else None)
     ws = torch.empty(4 * Q.qm_moment_row_count(1 << 30), dtype=torch.float64, device="cuda")
     rec("moments_f64_2^30", lambda: Q.qm_moments(tt, 4, rows=ws), 1 << 30, 8)
     del zn, tt
@@ -236,13 +252,14 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     strikes = list(np.linspace(50, 150, 17))
     rows = torch.empty((Q.qm_mc_row_count(1 << 34), 34), dtype=torch.float64, device="cuda")
     rec("mc_call_sweep_f32_2^34_17K",
-        lambda: Q.qm_mc_european_call(1 << 34, SEED, 0, 100.0, 0.05, 0.2, 1.0, strikes, out=rows), 1 << 34, 0)
+        lambda: Q.qm_mc_european_call(1 << 34, SEED, 0, 100.0, 0.05, 0.2, 1.0, strikes, out=rows), 1 << 34, 0,
+        fact="mc")
     del rows
     # config 1: 2^20 fp64, breakless vs branching baselines (tail-stratified input)
     u1 = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
     z1 = torch.empty_like(u1)
     for name, alg in [("breakless_D13", Q.BREAKLESS), ("as241", Q.AS241), ("acklam", Q.ACKLAM),
-                      ("acklam_refined", Q.ACKLAM_REFINED), ("breakless77", Q.BREAKLESS77)]:
+                      ("acklam_refined", Q.ACKLAM_REFINED), ("moro", Q.MORO), ("breakless77", Q.BREAKLESS77)]:
         rec(f"config1_f64_2^20_{name}", lambda alg=alg: Q.qm_normal_quantile(u1, out=z1, alg=alg), 1 << 20, 16)
     del u64, z64
     return out
@@ -302,11 +319,13 @@ def run_ours(args):
 
     # roofline of the (only) kernel of the step: 8 algorithmic bytes per sample
     achieved = 8.0 * n / (ms_step / 1e3) / 1e9
-    traffic = load_traffic().get("k_normal_f32", {}).get("dram_bytes_per_elem")
+    fact = load_traffic().get("stream_f32", {})
+    traffic = fact.get("dram_bytes_per_elem")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": (traffic * n if traffic else None),
-            "kernel": "qm::k_normal_f32<ALG_BREAKLESS>", "algorithmic_bytes_per_launch": 8 * n,
-            "peak_source": peaks["source"]}
+            "kernel": "qm::k_normal_f32_tl<ALG_BREAKLESS, TlCfgL> (TMA bulk loads in, streaming stores out)",
+            "algorithmic_bytes_per_launch": 8 * n, "peak_source": peaks["source"],
+            "traffic_source": fact.get("source")}
 
     # e2e through the public C-ABI host entry point: pinned host in, pinned host out
     uh = torch.empty(n, dtype=torch.float32, pin_memory=True)

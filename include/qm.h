@@ -56,10 +56,15 @@ typedef enum { QM_F32 = 1, QM_F64 = 2 } qm_precision;
  *                  App C) or 86.75 (fp64, App D).  Keeps the precision in
  *                  the deep tail (u < 4.3e-17 in fp32, u < 1e-38 in fp64) at no
  *                  cost elsewhere (warp-uniform switch).  Normal quantile,
- *                  antithetic and exponential-base entry points. */
+ *                  antithetic and exponential-base entry points.
+ *  QM_MORO         Moro's quantile (Beasley-Springer centre for |u - 1/2| < 0.42,
+ *                  a log(log) series beyond; "Moro: breaks at u = 0.92", P:436,
+ *                  P:551), a further branching comparison kernel (
+ *                  coefficients external, R17); fp64 only, normal
+ *                  quantile entry point only. */
 typedef enum {
     QM_BREAKLESS = 0, QM_BREAKLESS77 = 1, QM_AS241 = 2, QM_ACKLAM = 3, QM_ACKLAM_REFINED = 4,
-    QM_BREAKLESS_TAIL = 5
+    QM_BREAKLESS_TAIL = 5, QM_MORO = 6
 } qm_algorithm;
 
 int         qm_abi_version(void);

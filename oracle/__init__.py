@@ -75,6 +75,7 @@ def lib():
             "orc_Q_taylor_coeffs": (None, [P]),
             "orc_normal_as241": (i32, [P, P, i64, i32]),
             "orc_normal_acklam": (i32, [P, P, i64, i32, i32]),
+            "orc_normal_moro": (i32, [P, P, i64, i32]),
             "orc_student_coeffs_ld": (i32, [dbl, i32, P]),
             "orc_student_tail_const": (None, [dbl, P]),
             "orc_student_crossover": (dbl, [dbl, i32, P]),
@@ -255,6 +256,13 @@ def normal_as241(u, prec: int = 64) -> np.ndarray:
 def normal_acklam(u, prec: int = 64, refine: bool = False) -> np.ndarray:
     u = _in(u); o = np.empty(u.shape, np.longdouble)
     _chk(lib().orc_normal_acklam(_p(u), _p(o), u.size, prec, int(refine)))
+    return o
+
+
+def normal_moro(u, prec: int = 64) -> np.ndarray:
+    """Moro (1995) quantile (row f4), same formula, long double."""
+    u = _in(u); o = np.empty(u.shape, np.longdouble)
+    _chk(lib().orc_normal_moro(_p(u), _p(o), u.size, prec))
     return o
 
 

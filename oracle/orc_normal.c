@@ -427,6 +427,52 @@ int orc_normal_acklam(const double *u, ld *out, int64_t n, int prec, int refine)
     return 0;
 }
 
+/* --------------------------------------------------------------------------
+ * Moro (1995), the Beasley-Springer central rational with Moro's tail series
+ * ("Moro: breaks at u = 0.92"; "In the Moro model a log(log()) operation
+ * is carried out in the tail region").  Coefficients are
+ * NOT in the paper (reading R17): transcribed from Moro's publication, pinned by
+ * its published accuracy (absolute error < 3e-9 for |x| <= 7) in the tests.
+ *   y = u - 1/2;  |y| < 0.42:  x = y A(y^2) / B(y^2)   (A cubic, B quartic, B(0) = 1)
+ *   else          r = min(u, 1-u), s = log(-log r), x = +-C(s)  (C degree 8),
+ *                 negative for u < 1/2.
+ * ------------------------------------------------------------------------ */
+static const char *MO_A[4] = { "2.50662823884", "-18.61500062529", "41.39119773534", "-25.44106049637" };
+static const char *MO_B[5] = { "1", "-8.47351093090", "23.08336743743", "-21.06224101826", "3.13082909833" };
+static const char *MO_C[9] = { "0.3374754822726147", "0.9761690190917186", "0.1607979714918209",
+    "0.0276438810333863", "0.0038405729373609", "0.0003951896511919", "0.0000321767881768",
+    "0.0000002888167364", "0.0000003960315187" };
+
+/* ascending powers: c[0] + c[1] x + ... */
+static ld horner_up(const char **c, int n, int prec, ld x)
+{
+    ld s = coef(c[n - 1], prec);
+    for (int i = n - 2; i >= 0; --i) s = s * x + coef(c[i], prec);
+    return s;
+}
+
+static ld moro_one(ld u, int prec)
+{
+    if (isnan(u) || u < 0.0L || u > 1.0L) return NAN;
+    if (u == 0.0L) return -INFINITY;
+    if (u == 1.0L) return INFINITY;
+    double yd = (double)u - 0.5;                        /* decision in double */
+    ld y = u - 0.5L;
+    if (fabs(yd) < 0.42) {
+        ld r = y * y;
+        return y * horner_up(MO_A, 4, prec, r) / horner_up(MO_B, 5, prec, r);
+    }
+    ld t = (y < 0.0L) ? u : 1.0L - u;                   /* exact */
+    ld x = horner_up(MO_C, 9, prec, logl(-logl(t)));
+    return (y < 0.0L) ? -x : x;
+}
+
+int orc_normal_moro(const double *u, ld *out, int64_t n, int prec)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = moro_one((ld)u[i], prec);
+    return 0;
+}
+
 /* Q(v) of App C with float-rounded coefficients (for orc_mc.c) */
 ld orc_Q_C55_f32coef(ld v)
 {

@@ -17,7 +17,7 @@
 
 namespace qm {
 
-enum { ALG_AS241 = 2, ALG_ACKLAM = 3, ALG_ACKLAM_REF = 4 };
+enum { ALG_AS241 = 2, ALG_ACKLAM = 3, ALG_ACKLAM_REF = 4, ALG_MORO = 6 };
 
 // AS241 PPND16 in ascending powers
 __constant__ double kAS_A[8] = {3.3871328727963666080e0, 1.3314166789178437745e+2, 1.9715909503065514427e+3,
@@ -109,9 +109,39 @@ QM_DEV double acklam(double p)
     return (p < 0.5) ? x : 0.0 - x;
 }
 
+// Moro (1995): Beasley-Springer central rational y A(y^2)/B(y^2) for
+// |y| = |u - 1/2| < 0.42 ("Moro: breaks at u = 0.92"), Moro's series in
+// s = log(-log r), r = min(u, 1-u), beyond ("a log(log()) operation is carried
+// out in the tail region").  Coefficients external (R17), ascending.
+__constant__ double kMO_A[4] = {2.50662823884, -18.61500062529, 41.39119773534, -25.44106049637};
+__constant__ double kMO_B[5] = {1.0, -8.47351093090, 23.08336743743, -21.06224101826, 3.13082909833};
+__constant__ double kMO_C[9] = {0.3374754822726147, 0.9761690190917186, 0.1607979714918209,
+                                0.0276438810333863, 0.0038405729373609, 0.0003951896511919,
+                                0.0000321767881768, 0.0000002888167364, 0.0000003960315187};
+
+QM_DEV double moro(double u)
+{
+    if (!(u >= 0.0 && u <= 1.0)) return nan_d();
+    if (u == 0.0) return -inf_d();
+    if (u == 1.0) return inf_d();
+    const double yd = __dadd_rn(u, -0.5);
+    if (fabs(yd) < 0.42) {
+        const dd y = two_sum(u, -0.5);                              // exact y
+        const dd r = dd_mul(y, y);
+        return dd_div_round(dd_mul(y, horner_dd<4>(kMO_A, r)), horner_dd<5>(kMO_B, r));
+    }
+    const double t = (yd < 0.0) ? u : __dadd_rn(1.0, -u);          // exact
+    const dd L = neg_log_dd(t);                                     // -log t > 0
+    const dd sl = dd_add_d(dd_log(L.hi), L.lo / L.hi);              // log(L_hi + L_lo)
+    const dd x = horner_dd<9>(kMO_C, sl);
+    const double xr = __dadd_rn(x.hi, x.lo);
+    return (yd < 0.0) ? -xr : xr;
+}
+
 template <int ALG>
 QM_DEV double branchy(double u)
 {
+    if (ALG == ALG_MORO) return moro(u);
     if (ALG == ALG_AS241) return as241(u);
     if (ALG == ALG_ACKLAM) return acklam<false>(u);
     return acklam<true>(u);

@@ -162,7 +162,7 @@ qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
     return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
 }
 
-#define QM_ALG_LAST QM_BREAKLESS_TAIL
+#define QM_ALG_LAST QM_MORO
 
 bool breakless_family(qm_algorithm a) { return a == QM_BREAKLESS || a == QM_BREAKLESS77 || a == QM_BREAKLESS_TAIL; }
 
@@ -215,6 +215,7 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     case QM_ACKLAM_REFINED:
         k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n);
         return launched();
+    case QM_MORO: k_branchy_f64<ALG_MORO><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n); return launched();
     default: break;
     }
     const int g = grid_for(n, kThreads * 2, 8);

@@ -163,7 +163,14 @@ QM_DEV float rational_f32path(float z, const double *P, const double *Q)
     double t = __dmul_rn(p, r);
     const double e = __fma_rn(-q, t, p);
     t = __fma_rn(e, r, t);
+#ifdef QM_F32_FINAL_DMUL
     return (float)__dmul_rn(zd, t);
+#else
+    // z (P/Q) with P/Q rounded to float and the product in fp32: one DMUL fewer
+    // on the FP64 pipe (the kernel's co-bottleneck) for +0.5 ulp: <= 2.41 ulp over
+    // the fp32 grid in emulation (final DMUL: 1.67)
+    return __fmul_rn(__double2float_rn(t), z);
+#endif
 }
 
 // copysign by the sign of (u - (1-u)): +0 at u = 1/2 (P:773, P:855 sgn = +1)

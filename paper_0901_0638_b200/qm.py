@@ -12,8 +12,8 @@ import torch
 
 from . import _lib as L
 
-BREAKLESS, BREAKLESS77, AS241, ACKLAM, ACKLAM_REFINED, BREAKLESS_TAIL = (
-    L.QM_BREAKLESS, L.QM_BREAKLESS77, L.QM_AS241, L.QM_ACKLAM, L.QM_ACKLAM_REFINED, L.QM_BREAKLESS_TAIL)
+BREAKLESS, BREAKLESS77, AS241, ACKLAM, ACKLAM_REFINED, BREAKLESS_TAIL, MORO = (
+    L.QM_BREAKLESS, L.QM_BREAKLESS77, L.QM_AS241, L.QM_ACKLAM, L.QM_ACKLAM_REFINED, L.QM_BREAKLESS_TAIL, L.QM_MORO)
 
 
 def _prec(t: torch.Tensor) -> int:

@@ -126,11 +126,14 @@ def test_exp_to_normal(dtype, alg, formula, prec, bar):
 
 
 # -------------------------------------------------- comparison quantiles (a5)
-@pytest.mark.parametrize("alg,name", [(Q.AS241, "as241"), (Q.ACKLAM, "acklam")])
+@pytest.mark.parametrize("alg,name", [(Q.AS241, "as241"), (Q.ACKLAM, "acklam"), (Q.MORO, "moro")])
 def test_branchy_baselines(alg, name):
     u = I.mixed_uniforms((1 << 18) + 11, dtype=np.float64)
+    if name == "moro":   # both sides of Moro's break and its neighbourhood
+        u = np.concatenate([u, 0.08 + np.linspace(-1e-9, 1e-9, 101), 0.92 + np.linspace(-1e-9, 1e-9, 101)])
     g = _gpu(Q.qm_normal_quantile, u, alg=alg)
-    ref = O.normal_as241(u.astype(np.float64), 64) if name == "as241" else O.normal_acklam(u, 64, False)
+    ref = {"as241": lambda: O.normal_as241(u, 64), "acklam": lambda: O.normal_acklam(u, 64, False),
+           "moro": lambda: O.normal_moro(u, 64)}[name]()
     err = ulp_errors(g, ref, np.float64)
     assert err.max() <= 2.0, summary(err)
 

@@ -261,3 +261,36 @@ def test_refined_acklam():
     assert (np.abs(r - ex) / np.maximum(1.0, np.abs(ex))).max() < 1e-17
     l1 = O.normal_acklam(u, 64, False)
     assert np.median(np.abs(r - ex) / np.abs(l1 - ex + 1e-300)) < 1e-6   # the step helps
+
+
+# ------------------------------------------------- Moro comparison quantile (f4)
+def test_moro_published_accuracy():
+    """Moro (1995) publishes an absolute error below 3e-9 out to seven standard
+    deviations (external, reading R17; a wrong digit in any of the 17 transcribed
+    coefficients breaks it).  The worst case sits at the break u = 0.08 / 0.92,
+    where the paper says Moro breaks."""
+    lo = 1.2798125438858e-12                                  # Phi(-7)
+    u = np.concatenate([np.linspace(lo, 1 - 1e-10, 200001), np.exp(np.linspace(np.log(lo), np.log(0.5), 20001)),
+                        [0.08 - 1e-12, 0.08 + 1e-12, 0.92 - 1e-12, 0.92 + 1e-12]])
+    e = np.abs(O.normal_moro(u, 64) - O.ndtri_exact(u)).astype(float)
+    assert e.max() < 3.1e-9
+    assert e.max() > 2.5e-9                                   # nearly attained
+    i = np.argmax(e)
+    assert abs(min(u[i], 1 - u[i]) - 0.08) < 1e-3             # at the break
+
+
+def test_moro_regions_and_symmetry():
+    """Central rational for |u - 1/2| < 0.42, log(log) tail beyond (P:436, P:551);
+    odd symmetry w(1-u) = -w(u) on exact pairs; specials as the other quantiles."""
+    k = np.arange(1, 2000, dtype=np.float64)
+    u = k / 4096.0
+    a, b = O.normal_moro(u, 64), O.normal_moro(1 - u, 64)
+    assert np.array_equal(a, -b)
+    # the two branches agree at the break to the method's accuracy (continuity)
+    lo = O.normal_moro(np.array([0.08 + 2 ** -40]), 64)[0]
+    hi = O.normal_moro(np.array([0.08 - 2 ** -40]), 64)[0]
+    assert abs(lo - hi) < 1e-8
+    sp = O.normal_moro(np.array([0.0, 1.0, 0.5, -0.1, 1.1, np.nan]), 64)
+    assert sp[0] == -np.inf and sp[1] == np.inf and sp[2] == 0 and not np.signbit(sp[2])
+    assert np.all(np.isnan(sp[3:]))
+

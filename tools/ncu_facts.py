@@ -1,0 +1,27 @@
+"""profiles/<round>/ncu_*.json -> profiles/ncu_traffic.json: per-sample DRAM bytes and
+warp-instructions of each hot-path kernel (bench.py reads it for `roofline.traffic`
+and the issue-slot rooflines of the compute-bound rows).
+
+    python tools/ncu_facts.py profiles/r02
+"""
+import json
+import os
+import sys
+
+# elements per captured launch (tools/prof_kernel.py)
+ELEMS = {"stream_f32": 1 << 28, "stream_f32_ldg": 1 << 28, "stream_f64": 1 << 28, "fused_f32": 1 << 32,
+         "fused_f64": 1 << 31, "student": 1 << 30, "exp2n_f32": 1 << 28, "moments": 1 << 30, "mc": 1 << 32}
+
+d = sys.argv[1]
+out = {}
+for name, n in ELEMS.items():
+    p = os.path.join(d, f"ncu_{name}.json")
+    if not os.path.exists(p):
+        continue
+    k = json.load(open(p))[0]
+    out[name] = {"kernel": k["kernel"],
+                 "dram_bytes_per_elem": (k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0)) / n,
+                 "warp_inst_per_elem": k.get("warp_inst_executed", 0) / n,
+                 "source": f"{p} (ncu --set full, one launch of {n} samples)"}
+json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
+print(json.dumps(out, indent=1))

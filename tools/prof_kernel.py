@@ -28,7 +28,8 @@ elif name == "fused_f64":
 elif name.startswith("config1_"):
     import numpy as np
     from synth import inputs as I
-    alg = {"breakless": Q.BREAKLESS, "as241": Q.AS241, "acklam": Q.ACKLAM, "refined": Q.ACKLAM_REFINED}[name[8:]]
+    alg = {"breakless": Q.BREAKLESS, "as241": Q.AS241, "acklam": Q.ACKLAM, "refined": Q.ACKLAM_REFINED,
+           "moro": Q.MORO}[name[8:]]
     u = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
     z = torch.empty_like(u)
     fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
