@@ -225,6 +225,14 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64, out=u64)
     z64 = torch.empty_like(u64)
     rec("stream_f64_D13_2^28", lambda: Q.qm_normal_quantile(u64, out=z64), n, 16, fact="stream_f64")
+    # rows f3/f4: (12,12) fp64 on [0, 37], (8,8) fp32 on [0, 74], two-region fp32
+    rec("stream_f64_F1212_2^28", lambda: Q.qm_normal_quantile(u64, out=z64, alg=Q.BREAKLESS1212), n, 16)
+    u32 = torch.empty(n, dtype=torch.float32, device="cuda")
+    Q.qm_philox_uniform(n, SEED, 0, out=u32)
+    z32 = torch.empty_like(u32)
+    rec("stream_f32_F88_2^28", lambda: Q.qm_normal_quantile(u32, out=z32, alg=Q.BREAKLESS88), n, 8)
+    rec("stream_f32_two_region_2^28", lambda: Q.qm_normal_quantile(u32, out=z32, alg=Q.TWO_REGION), n, 8)
+    del u32, z32
     zf = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
     rec("philox_fused_f32_2^32", lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=zf), 1 << 32, 4, fact="fused_f32")
     del zf

@@ -61,10 +61,23 @@ typedef enum { QM_F32 = 1, QM_F64 = 2 } qm_precision;
  *                  a log(log) series beyond; "Moro: breaks at u = 0.92", P:436,
  *                  P:551), a further branching comparison kernel (
  *                  coefficients external, R17); fp64 only, normal
- *                  quantile entry point only. */
+ *                  quantile entry point only.
+ *  QM_BREAKLESS1212  (12,12) single patch on v in [0, 37], max relative error
+ *                  4.85e-16 ("a (12,12) rational approximation exists ... less than
+ *                  5e-16"); fp64 only.
+ *  QM_BREAKLESS88  (8,8) single patch on v in [0, 74], 5.75e-10 ("precision about
+ *                  6e-10 on the range 0 <= v <= 74"); fp32 and fp64 (row f3).
+ *  QM_TWO_REGION   (4,4) below v = 10, App C (5,5) above: the two-region variant of
+ *                  P:664 ("shorter rational approximations in two regions"); max
+ *                  error 3.62e-7 (App C's); fp32 only (row f4).  The branch is a
+ *                  warp-uniform vote: a warp with every lane below the break runs
+ *                  the short rational only.
+ *  The f3/f4 coefficients are our own minimax fits (the paper does not print
+ *  them): tests/golden/fit_12_37.txt, fit_8_74.txt, fit_4_10.txt.  These three
+ *  are normal-quantile (qm_normal_quantile, qm_normal_quantile_host) only. */
 typedef enum {
     QM_BREAKLESS = 0, QM_BREAKLESS77 = 1, QM_AS241 = 2, QM_ACKLAM = 3, QM_ACKLAM_REFINED = 4,
-    QM_BREAKLESS_TAIL = 5, QM_MORO = 6
+    QM_BREAKLESS_TAIL = 5, QM_MORO = 6, QM_BREAKLESS1212 = 7, QM_BREAKLESS88 = 8, QM_TWO_REGION = 9
 } qm_algorithm;
 
 int         qm_abi_version(void);

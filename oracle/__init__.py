@@ -31,6 +31,7 @@ _SRCS = ["orc_philox.c", "orc_normal.c", "orc_student.c", "orc_moments.c", "orc_
 
 # formula ids of the oracle (local to the oracle; the product has its own enum)
 C55, A77, D13 = 55, 77, 13
+F1212, F88, F44, TWO_REGION = 1212, 88, 44, 410   # our fits (row f3) and the two-region variant (f4)
 
 
 def build(force: bool = False) -> Path:
@@ -161,7 +162,8 @@ def Q_exact(v) -> np.ndarray:
 
 
 def rational(v, formula: int, prec: int) -> np.ndarray:
-    """v P(v)/Q(v) of formula C55/A77/D13; prec 32/64 rounds the coefficients, 0 keeps decimals."""
+    """v P(v)/Q(v) of formula C55/A77/D13/F1212/F88/F44/TWO_REGION; prec 32/64 rounds the
+    coefficients, 0 keeps decimals."""
     v = _in(v, np.longdouble); o = np.empty(v.shape, np.longdouble)
     _chk(lib().orc_rational(_p(v), _p(o), v.size, formula, prec))
     return o

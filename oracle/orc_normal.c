@@ -35,6 +35,10 @@
 #define ORC_C55 55
 #define ORC_A77 77
 #define ORC_D13 13
+#define ORC_F1212 1212   /* (12,12) on [0, 37] */
+#define ORC_F88 88       /* (8,8) on [0, 74] */
+#define ORC_F44 44       /* (4,4) on [0, 10], first region of the two-region variant */
+#define ORC_TWO 410      /* two regions: F44 for v < 10, App C (5,5) for v >= 10 */
 /* coefficient precision: 32 = float-rounded, 64 = double-rounded, 0 = decimal */
 
 /* App A / App B (7,7): P:477-497 (numerator), P:485-497 (denominator) */
@@ -67,6 +71,43 @@ static const char *D13_Q[14] = {
     "0.00014919732843986856251", "2.7477061392049947066e-6", "2.2815008011613816939e-8",
     "7.0445790305953963457e-11", "5.1535907808963289678e-14" };
 
+/* Our minimax fits (tools/fit_rational.py), transcribed from
+ * tests/golden/fit_*.txt: the (12,12) on [0,37] and (8,8) on [0,74] the paper
+ * says exist, and the (4,4) on [0,10] of the two-region variant. */
+static const char *F1212_P[13] = {
+    "1.25331413731549964304885084933", "5.65670727193097123052913156555",
+    "10.199184028049004645639650354", "9.49108178418734942631477139003",
+    "4.94304333170547437473236493918", "1.47293406972979776643830812522",
+    "0.249077147187243284286425789887", "0.0232075251548776468184535573962",
+    "0.00113211638446441623489197365915", "0.000026638805014702015041938526811",
+    "0.000000262823263993221383793586115962", "8.20115160731597726774034377471e-10",
+    "3.4080843072305026219786124261e-13" };
+static const char *F1212_Q[13] = {
+    "1.0", "5.01339939725483198543174978089", "10.2160051129404404259102375667",
+    "10.9670844662824747543017650822", "6.74844347326083628169062975985",
+    "2.44148341873030012307321591735", "0.516866979805929966868864954603",
+    "0.0624322209086865620690205639678", "0.00411740318775822728331972658499",
+    "0.00013852471353158268838850038814", "0.00000213335696590330667438560151822",
+    "0.0000000123741421877613097338506656296", "1.71840938834726185281010719498e-11" };
+static const char *F88_P[9] = {
+    "1.25331413659487693200589460544", "3.18279215828640909853465485323",
+    "2.69637013151484046914318369988", "0.926505960348117503759109131467",
+    "0.130722564999804748080717604434", "0.00715510742068364856695515828894",
+    "0.000134566885939144919435102866116", "0.000000669320737492863356757758585237",
+    "3.78894005999045094010072867485e-10" };
+static const char *F88_Q[9] = {
+    "1.0", "3.03950064147177248702038516122", "3.24267820535186536296356820427",
+    "1.49261049909605991213659399514", "0.302049532338050455259987910733",
+    "0.0255324575872787421879918341977", "0.000815155781723673184564102970288",
+    "0.00000817923481671560569243134101007", "0.0000000166707331365471438381381542416" };
+static const char *F44_P[5] = {
+    "1.25331376367946351584057665416", "1.90154131297345796677471850561",
+    "0.692706016566279324284406456679", "0.0560005883011708193276104273226",
+    "0.000448739389131331445037989032119" };
+static const char *F44_Q[5] = {
+    "1.0", "2.01718797443210201360154517184", "1.13309652308639082468928923168",
+    "0.179982309491888788965156666547", "0.0053418912252851127623755674913" };
+
 static ld coef(const char *s, int prec)
 {
     if (prec == 32) return (ld)(float)strtod(s, NULL);   /* `const float P1 = <double literal>;` */
@@ -74,15 +115,29 @@ static ld coef(const char *s, int prec)
     return strtold(s, NULL);                             /* decimal, for exact-arithmetic bounds */
 }
 
-typedef struct { int n; ld p[14]; ld q[14]; } rat_t;
+/* one rational, or (two-region formula) a second one used for v >= vb */
+typedef struct { int n; ld p[14]; ld q[14]; int n2; ld vb; ld p2[14]; ld q2[14]; } rat_t;
+#define ORC_TWO_BREAK 10.0L
 
 static int get_rat(int formula, int prec, rat_t *r)
 {
     const char **P, **Q; int n;
+    r->n2 = 0;
+    if (formula == ORC_TWO) {            /* (4,4) below the break, App C above */
+        rat_t hi;
+        get_rat(ORC_C55, prec, &hi);
+        get_rat(ORC_F44, prec, r);
+        r->n2 = hi.n; r->vb = ORC_TWO_BREAK;
+        for (int i = 0; i < hi.n; ++i) { r->p2[i] = hi.p[i]; r->q2[i] = hi.q[i]; }
+        return 0;
+    }
     switch (formula) {
     case ORC_A77: P = A77_P; Q = A77_Q; n = 8; break;
     case ORC_C55: P = C55_P; Q = C55_Q; n = 6; break;
     case ORC_D13: P = D13_P; Q = D13_Q; n = 14; break;
+    case ORC_F1212: P = F1212_P; Q = F1212_Q; n = 13; break;
+    case ORC_F88: P = F88_P; Q = F88_Q; n = 9; break;
+    case ORC_F44: P = F44_P; Q = F44_Q; n = 5; break;
     default: return -1;
     }
     r->n = n;
@@ -93,8 +148,11 @@ static int get_rat(int formula, int prec, rat_t *r)
 /* Q(v) = v * P(v) / Q(v), nested (Horner) form as printed. */
 static ld rational_Q(const rat_t *r, ld v)
 {
-    ld P = r->p[r->n - 1], Q = r->q[r->n - 1];
-    for (int i = r->n - 2; i >= 0; --i) { P = r->p[i] + v * P; Q = r->q[i] + v * Q; }
+    const int second = r->n2 > 0 && v >= r->vb;
+    const int n = second ? r->n2 : r->n;
+    const ld *p = second ? r->p2 : r->p, *q = second ? r->q2 : r->q;
+    ld P = p[n - 1], Q = q[n - 1];
+    for (int i = n - 2; i >= 0; --i) { P = p[i] + v * P; Q = q[i] + v * Q; }
     return v * P / Q;
 }
 

@@ -16,6 +16,7 @@ LIB_PATH = Path(os.environ.get("QM_LIB_PATH", str(_HERE / "libqm.so")))
 QM_OK, QM_EINVAL, QM_EUNSUPPORTED, QM_ECUDA = 0, 1, 2, 3
 QM_F32, QM_F64 = 1, 2
 QM_BREAKLESS, QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED, QM_BREAKLESS_TAIL, QM_MORO = 0, 1, 2, 3, 4, 5, 6
+QM_BREAKLESS1212, QM_BREAKLESS88, QM_TWO_REGION = 7, 8, 9
 QM_MOMENT_CHUNK = 65536
 QM_MC_CHUNK = 1 << 20
 QM_TARGET_HYPERBOLIC, QM_TARGET_VG = 1, 2

@@ -132,6 +132,8 @@ char tl_cfg()
 template <int ALG>
 qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
 {
+    if constexpr (ALG != ALG_BREAKLESS)     // A/B shapes only for the headline formula
+        return launch_stream_f32<TlCfgL>(k_normal_f32_tl<ALG, TlCfgL>, k_normal_f32<ALG>, u, z, n, s);
     if (stream_path() == 2) {
         switch (tl_cfg()) {
         case 'K': return launch_stream_f32<TlCfgK>(k_normal_f32_tl<ALG, TlCfgK>, k_normal_f32<ALG>, u, z, n, s);
@@ -162,9 +164,16 @@ qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
     return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
 }
 
-#define QM_ALG_LAST QM_MORO
+#define QM_ALG_LAST QM_TWO_REGION
 
 bool breakless_family(qm_algorithm a) { return a == QM_BREAKLESS || a == QM_BREAKLESS77 || a == QM_BREAKLESS_TAIL; }
+
+// which algorithms qm_normal_quantile evaluates in which precision (qm.h)
+bool normal_supported(qm_precision p, qm_algorithm a)
+{
+    if (p == QM_F32) return breakless_family(a) || a == QM_BREAKLESS88 || a == QM_TWO_REGION;
+    return a != QM_TWO_REGION;
+}
 
 // f(std::integral_constant<int, ALG>) for the breakless family, else QM_EUNSUPPORTED
 template <typename F>
@@ -202,11 +211,15 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;
     if (p != QM_F32 && p != QM_F64) return QM_EINVAL;
     if (alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (!normal_supported(p, alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int vec = aligned16(u) && aligned16(z);
-    if (p == QM_F32)
+    if (p == QM_F32) {
+        if (alg == QM_BREAKLESS88) return normal_f32<ALG_F88>((const float *)u, (float *)z, n, s);
+        if (alg == QM_TWO_REGION) return normal_f32<ALG_TWO_REGION>((const float *)u, (float *)z, n, s);
         return with_breakless(alg, [&](auto A) { return normal_f32<decltype(A)::value>((const float *)u, (float *)z, n, s); });
+    }
     const double *ud = (const double *)u;
     double *zd = (double *)z;
     switch (alg) {
@@ -216,6 +229,13 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
         k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n);
         return launched();
     case QM_MORO: k_branchy_f64<ALG_MORO><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n); return launched();
+    case QM_BREAKLESS1212:
+        k_normal_f64<ALG_F1212><<<grid_for(n, kThreads * 2, 8), kThreads, 0, s>>>(ud, zd, n, vec);
+        return launched();
+    case QM_BREAKLESS88:
+        k_normal_f64<ALG_F88><<<grid_for(n, kThreads * 2, 8), kThreads, 0, s>>>(ud, zd, n, vec);
+        return launched();
+    case QM_TWO_REGION: return QM_EUNSUPPORTED;
     default: break;
     }
     const int g = grid_for(n, kThreads * 2, 8);
@@ -472,7 +492,7 @@ qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, q
 {
     if (n < 0 || bad_ptrs(u_host, z_host, n) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
     if (alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
-    if (p == QM_F32 && !breakless_family(alg)) return QM_EUNSUPPORTED;
+    if (!normal_supported(p, alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     const size_t es = (p == QM_F32) ? 4 : 8;
     const int64_t chunk = (int64_t)1 << 24;                 // elements per pipeline stage

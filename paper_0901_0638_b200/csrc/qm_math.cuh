@@ -71,6 +71,57 @@ __constant__ double kD13Q[14] = {
     0.0040618506206078995821, 0.00014919732843986856251, 2.7477061392049947066e-6,
     2.2815008011613816939e-8, 7.0445790305953963457e-11, 5.1535907808963289678e-14};
 
+// Our minimax fits (tests/golden/fit_*.txt, tools/fit_rational.py; SURVEY rows
+// f3/f4): the (12,12) on [0, 37] (< 5e-16) and (8,8) on [0, 74] (~6e-10) that
+// P:544 says exist, and the (4,4) on [0, 10] below the break of the two-region
+// variant.  Double-rounded (fp64) and float-rounded (fp32) as for App A-D.
+__constant__ double kF12P[13] = {
+    1.25331413731549964304885084933, 5.65670727193097123052913156555, 10.199184028049004645639650354,
+    9.49108178418734942631477139003, 4.94304333170547437473236493918, 1.47293406972979776643830812522,
+    0.249077147187243284286425789887, 0.0232075251548776468184535573962,
+    0.00113211638446441623489197365915, 0.000026638805014702015041938526811,
+    0.000000262823263993221383793586115962, 8.20115160731597726774034377471e-10,
+    3.4080843072305026219786124261e-13};
+__constant__ double kF12Q[13] = {
+    1.0, 5.01339939725483198543174978089, 10.2160051129404404259102375667,
+    10.9670844662824747543017650822, 6.74844347326083628169062975985, 2.44148341873030012307321591735,
+    0.516866979805929966868864954603, 0.0624322209086865620690205639678,
+    0.00411740318775822728331972658499, 0.00013852471353158268838850038814,
+    0.00000213335696590330667438560151822, 0.0000000123741421877613097338506656296,
+    1.71840938834726185281010719498e-11};
+__constant__ double kF88P_d[9] = {
+    1.25331413659487693200589460544, 3.18279215828640909853465485323, 2.69637013151484046914318369988,
+    0.926505960348117503759109131467, 0.130722564999804748080717604434,
+    0.00715510742068364856695515828894, 0.000134566885939144919435102866116,
+    0.000000669320737492863356757758585237, 3.78894005999045094010072867485e-10};
+__constant__ double kF88Q_d[9] = {
+    1.0, 3.03950064147177248702038516122, 3.24267820535186536296356820427,
+    1.49261049909605991213659399514, 0.302049532338050455259987910733,
+    0.0255324575872787421879918341977, 0.000815155781723673184564102970288,
+    0.00000817923481671560569243134101007, 0.0000000166707331365471438381381542416};
+__constant__ double kF88P_f[9] = {
+    (double)(float)1.25331413659487693200589460544, (double)(float)3.18279215828640909853465485323,
+    (double)(float)2.69637013151484046914318369988, (double)(float)0.926505960348117503759109131467,
+    (double)(float)0.130722564999804748080717604434, (double)(float)0.00715510742068364856695515828894,
+    (double)(float)0.000134566885939144919435102866116,
+    (double)(float)0.000000669320737492863356757758585237,
+    (double)(float)3.78894005999045094010072867485e-10};
+__constant__ double kF88Q_f[9] = {
+    (double)(float)1.0, (double)(float)3.03950064147177248702038516122,
+    (double)(float)3.24267820535186536296356820427, (double)(float)1.49261049909605991213659399514,
+    (double)(float)0.302049532338050455259987910733, (double)(float)0.0255324575872787421879918341977,
+    (double)(float)0.000815155781723673184564102970288,
+    (double)(float)0.00000817923481671560569243134101007,
+    (double)(float)0.0000000166707331365471438381381542416};
+__constant__ double kF44P_f[5] = {
+    (double)(float)1.25331376367946351584057665416, (double)(float)1.90154131297345796677471850561,
+    (double)(float)0.692706016566279324284406456679, (double)(float)0.0560005883011708193276104273226,
+    (double)(float)0.000448739389131331445037989032119};
+__constant__ double kF44Q_f[5] = {
+    (double)(float)1.0, (double)(float)2.01718797443210201360154517184,
+    (double)(float)1.13309652308639082468928923168, (double)(float)0.179982309491888788965156666547,
+    (double)(float)0.0053418912252851127623755674913};
+
 // fp32 log: log1p(f) = f + f^2 R(f), f in [-1/3, 1/3); R: degree-7 Chebyshev fit
 // (tools/fit_log.py), |error of R| < 2.1e-7.  Where the log's relative error
 // reaches z unscaled (e = 0, f -> -1/3) it is < 0.3 ulp of z; the fp32 map stays
@@ -270,16 +321,25 @@ QM_DEV double apply_sign_f64(double mag, double u, double omu)
 // supplementary tail model beyond; vc = 37 for App C and
 // 86.75 for App D (reading R23).  Its fast path is ALG_BREAKLESS: the warp vote
 // sends a warp with any v >= vc to the careful path.
-enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5 };
+// ALG_F1212 / ALG_F88 / ALG_TWO_REGION: rows f3/f4 (our fits); ALG_F44 is the
+// fast path of the two-region variant (every lane of the warp below the break).
+enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5, ALG_F1212 = 7, ALG_F88 = 8,
+       ALG_TWO_REGION = 9, ALG_F44 = 10 };
+#define QM_TWO_BREAK_F32 10.0f
 #define QM_VC_F32 37.0f
 #define QM_VC_F64 86.75
 
-template <int ALG> __host__ __device__ constexpr int fast_alg() { return ALG == ALG_BREAKLESS_TAIL ? ALG_BREAKLESS : ALG; }
+template <int ALG> __host__ __device__ constexpr int fast_alg()
+{
+    return ALG == ALG_BREAKLESS_TAIL ? ALG_BREAKLESS : ALG == ALG_TWO_REGION ? ALG_F44 : ALG;
+}
 // smallest vv = min(u, 1-u) of the fast path: normal numbers; for the tail
 // composite also v = -log(2 vv) < vc (e^-37/2 = 4.2665e-17, e^-86.75/2 = 1.0566e-38)
 template <int ALG> __host__ __device__ constexpr float fast_vv_min_f32()
 {
-    return ALG == ALG_BREAKLESS_TAIL ? 4.3e-17f : 1.17549435e-38f;
+    // two-region: z < 10 for every vv >= 2.2705e-5 (e^-10/2 = 2.26999e-5, margin for
+    // the fp32 log), so the whole warp is below the break
+    return ALG == ALG_BREAKLESS_TAIL ? 4.3e-17f : ALG == ALG_TWO_REGION ? 2.2705e-5f : 1.17549435e-38f;
 }
 template <int ALG> __host__ __device__ constexpr double fast_vv_min_f64()
 {
@@ -293,6 +353,10 @@ template <int ALG>
 QM_DEV float rat32(float z)
 {
     if (ALG == ALG_BREAKLESS77) return rational_f32path<8>(z, kA77P_f, kA77Q_f);
+    if (ALG == ALG_F88) return rational_f32path<9>(z, kF88P_f, kF88Q_f);
+    if (ALG == ALG_F44) return rational_f32path<5>(z, kF44P_f, kF44Q_f);
+    if (ALG == ALG_TWO_REGION)
+        return (z < QM_TWO_BREAK_F32) ? rational_f32path<5>(z, kF44P_f, kF44Q_f) : rational_f32path<6>(z, kC55P, kC55Q);
     if (ALG == ALG_BREAKLESS_TAIL) {
         const float r = rational_f32path<6>(z, kC55P, kC55Q);
         return (z < QM_VC_F32) ? r : (float)tail_model_q((double)z);
@@ -304,6 +368,8 @@ template <int ALG>
 QM_DEV double rat64(dd z)
 {
     if (ALG == ALG_BREAKLESS77) return rational_dd<8, 7>(z, kA77P_d, kA77Q_d);
+    if (ALG == ALG_F1212) return rational_dd<13, 12>(z, kF12P, kF12Q);
+    if (ALG == ALG_F88) return rational_dd<9, 8>(z, kF88P_d, kF88Q_d);
     if (ALG == ALG_BREAKLESS_TAIL)
         return (z.hi < QM_VC_F64) ? rational_dd<14, 10>(z, kD13P, kD13Q) : tail_model_q_dd(z);
     // compensating the last 10 of 13 Horner steps is enough: 0.65 ulp max over

@@ -14,6 +14,7 @@ from . import _lib as L
 
 BREAKLESS, BREAKLESS77, AS241, ACKLAM, ACKLAM_REFINED, BREAKLESS_TAIL, MORO = (
     L.QM_BREAKLESS, L.QM_BREAKLESS77, L.QM_AS241, L.QM_ACKLAM, L.QM_ACKLAM_REFINED, L.QM_BREAKLESS_TAIL, L.QM_MORO)
+BREAKLESS1212, BREAKLESS88, TWO_REGION = L.QM_BREAKLESS1212, L.QM_BREAKLESS88, L.QM_TWO_REGION
 
 
 def _prec(t: torch.Tensor) -> int:

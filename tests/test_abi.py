@@ -46,10 +46,13 @@ def test_argument_validation_before_launch(lib):
     assert lib.qm_normal_quantile(p, p, -1, L.QM_F32, 0, None) == L.QM_EINVAL
     assert lib.qm_normal_quantile(None, p, 5, L.QM_F32, 0, None) == L.QM_EINVAL
     assert lib.qm_normal_quantile(p, p, 5, 3, 0, None) == L.QM_EINVAL
-    assert lib.qm_normal_quantile(p, p, 5, L.QM_F32, 9, None) == L.QM_EINVAL
+    assert lib.qm_normal_quantile(p, p, 5, L.QM_F32, L.QM_TWO_REGION + 1, None) == L.QM_EINVAL
     assert lib.qm_normal_quantile(p, p, 5, L.QM_F32, L.QM_AS241, None) == L.QM_EUNSUPPORTED
     assert lib.qm_normal_quantile(p, p, 5, L.QM_F32, L.QM_MORO, None) == L.QM_EUNSUPPORTED
-    assert lib.qm_normal_quantile(p, p, 5, L.QM_F64, L.QM_MORO + 1, None) == L.QM_EINVAL
+    assert lib.qm_normal_quantile(p, p, 5, L.QM_F32, L.QM_BREAKLESS1212, None) == L.QM_EUNSUPPORTED
+    assert lib.qm_normal_quantile(p, p, 5, L.QM_F64, L.QM_TWO_REGION, None) == L.QM_EUNSUPPORTED
+    assert lib.qm_normal_quantile(p, p, 5, L.QM_F64, L.QM_TWO_REGION + 1, None) == L.QM_EINVAL
+    assert lib.qm_normal_antithetic(p, p, 4, L.QM_F32, L.QM_TWO_REGION, None) == L.QM_EUNSUPPORTED
     assert lib.qm_normal_philox(p, 5, L.QM_F64, L.QM_MORO, 1, 0, None) == L.QM_EUNSUPPORTED
     assert lib.qm_normal_quantile(p, p, 0, L.QM_F32, 0, None) == L.QM_OK       # n = 0: no-op
     assert lib.qm_normal_antithetic(p, p, 4, L.QM_F64, L.QM_ACKLAM, None) == L.QM_EUNSUPPORTED
