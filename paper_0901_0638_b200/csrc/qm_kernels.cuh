@@ -330,11 +330,10 @@ k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, in
 
 // --------------------------------------------------- Philox uniforms / fused
 // MODE 0: write the uniforms; MODE 1: write the normal quantile of them (fused).
-template <int MODE, int ALG>
-__global__ void __launch_bounds__(kThreads)
+template <int MODE, int ALG, int V = 2, int MINB = 1>   // V: Philox blocks per lane per chunk
+__global__ void __launch_bounds__(kThreads, MINB)
 k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
 {
-    constexpr int V = 2;                                  // Philox blocks per lane per chunk
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;

@@ -343,9 +343,27 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
     if (!student_params(nu, K, zstar, &sp)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const int g = grid_for(n, kThreads * 2, 8);
-    if (p == QM_F64) k_student_f64<<<g, kThreads, 0, s>>>((const double *)z, (double *)t, n, sp);
-    else k_student_f32<<<g, kThreads, 0, s>>>((const float *)z, (float *)t, n, sp);
+    int64_t done = 0;
+    if (p == QM_F64 && aligned16(z) && aligned16(t) && sp.kc == 3 && (K == 10 || K == 16)) {
+        // whole tiles through the TMA pipeline with the series unrolled at compile time
+        constexpr int64_t TILE = 2 * kStudentTileVecs;
+        const int64_t ntiles = n / TILE;
+        if (ntiles > 0) {
+            const size_t smem = (size_t)kStudentStages * kStudentTileVecs * 16;
+            auto k = (K == 10) ? k_student_f64_tl<10, 3> : k_student_f64_tl<16, 3>;
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return QM_ECUDA;
+            const int sms = sm_count_for_current_device();
+            const int64_t g = ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148);
+            k<<<(int)g, 32 * (kStudentNC + 1), smem, s>>>((const double *)z, (double *)t, ntiles, sp);
+            done = ntiles * TILE;
+        }
+    }
+    if (n > done) {
+        const int g = grid_for(n - done, kThreads * 2, 8);
+        if (p == QM_F64) k_student_f64<<<g, kThreads, 0, s>>>((const double *)z + done, (double *)t + done, n - done, sp);
+        else k_student_f32<<<g, kThreads, 0, s>>>((const float *)z, (float *)t, n, sp);
+    }
     return launched();
 }
 

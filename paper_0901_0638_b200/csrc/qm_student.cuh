@@ -15,6 +15,7 @@
 // the warp is in the tail (P(|z| > 3.9) ~ 1e-4 per sample).
 #pragma once
 #include "qm_dd.cuh"
+#include "qm_tma.cuh"
 
 #include "qm_student_params.h"
 
@@ -39,6 +40,31 @@ QM_DEV double student_central(const StudentParams &sp, double a)
     return __fma_rn(a, s, __dmul_rn(a, c));
 }
 
+// the same series with K and the compensated count KC fixed at compile time
+// (fully unrolled; bitwise equal to student_central for sp.K == K, sp.kc == KC)
+template <int K, int KC>
+QM_DEV double student_central_k(const StudentParams &sp, double a)
+{
+    const double yh = __dmul_rn(a, a);
+    const double yl = __fma_rn(a, a, -yh);
+    double s = sp.c[K], c = 0.0;
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+        if (i >= KC) {
+            s = __fma_rn(s, yh, sp.c[i]);
+        } else {
+            const double p = __dmul_rn(s, yh);
+            const double pi = __fma_rn(s, yh, -p);
+            const double t = __dadd_rn(p, sp.c[i]);
+            const double bb = __dadd_rn(t, -p);
+            const double sg = __dadd_rn(__dadd_rn(p, -__dadd_rn(t, -bb)), __dadd_rn(sp.c[i], -bb));
+            c = __fma_rn(c, yh, __fma_rn(s, yl, __dadd_rn(pi, sg)));
+            s = t;
+        }
+    }
+    return __fma_rn(a, s, __dmul_rn(a, c));
+}
+
 QM_DEV double student_tail(const StudentParams &sp, double a)
 {
     // log w = log(erfc(a/sqrt2)) + log(C_nu/2); erfc(x) = exp(-x^2) erfcx(x)
@@ -56,10 +82,11 @@ QM_DEV double student_tail(const StudentParams &sp, double a)
     return t.hi + t.lo;
 }
 
+template <int K = 0, int KC = 0>   // K = 0: run-time sp.K / sp.kc
 QM_DEV double student_map(const StudentParams &sp, double z, bool any_tail)
 {
     const double a = fabs(z);
-    double t = student_central(sp, a);
+    double t = (K > 0) ? student_central_k<K, KC>(sp, a) : student_central(sp, a);
     if (any_tail) {
         // every lane of the warp evaluates the tail at a >= z* (one erfcx region)
         const double tt = student_tail(sp, fmax(a, sp.zstar));
@@ -96,6 +123,38 @@ k_student_f32(const float *__restrict__ z, float *__restrict__ t, int64_t n, con
         const double r = student_map(sp, x, any);
         if (i < n) t[i] = (float)r;
     }
+}
+
+// fp64 through the TMA-in / streaming-store pipeline (qm_tma.cuh).  One vote per
+// 32 samples (one per element position of the lane's slice), as in k_student_f64:
+// the tail is expensive, so the vote granularity sets how often a warp pays it
+// (32 P(|z| >= z*) ~ 0.3 % of votes at nu = 4).
+template <int K, int KC>
+struct MapStudentF64 {
+    const StudentParams *sp;
+    QM_DEV double one(double x) const
+    {
+        const bool any = __any_sync(0xffffffffu, !(fabs(x) < sp->zstar));
+        return student_map<K, KC>(*sp, x, any);
+    }
+    template <int PER>
+    QM_DEV void map_slice(double2 *a) const
+    {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) a[j] = make_double2(one(a[j].x), one(a[j].y));
+    }
+};
+
+// 1 CTA/SM: a producer warp + 16 consumer warps, 4 stages of 32 KB (2048 double2)
+constexpr int kStudentNC = 16, kStudentStages = 4, kStudentTileVecs = 2048;
+
+template <int K, int KC>
+__global__ void __launch_bounds__(32 * (kStudentNC + 1), 1)
+k_student_f64_tl(const double *__restrict__ z, double *__restrict__ t, int64_t ntiles,
+                 const __grid_constant__ StudentParams sp)
+{
+    tma_load_map<double2, kStudentTileVecs, kStudentStages, kStudentNC>(
+        reinterpret_cast<const double2 *>(z), reinterpret_cast<double2 *>(t), ntiles, MapStudentF64<K, KC>{&sp});
 }
 
 }  // namespace qm

@@ -33,6 +33,22 @@ def test_student_parity(nu, K, zstar, dtype, bar):
     assert err.max() <= bar, summary(err)
 
 
+@pytest.mark.parametrize("nu,K,zstar", STUDENT)
+def test_student_pipeline_equals_generic_kernel(nu, K, zstar):
+    """fp64, 16-byte aligned, K in {10, 16}: whole 4096-sample tiles run through the
+    TMA pipeline with the series unrolled; a misaligned view runs the generic
+    kernel.  Both must agree bitwise (specials placed inside the tiles)."""
+    z = _z_inputs(np.float64)
+    z = np.concatenate([z[-11:], z[:-11]])
+    zd = torch.from_numpy(np.concatenate([[0.25], z])).cuda()
+    generic = Q.qm_recycle_normal_to_t(zd[1:], nu, K, zstar)          # 8-byte offset: misaligned
+    tiled = Q.qm_recycle_normal_to_t(zd[1:].clone(), nu, K, zstar)
+    assert torch.equal(generic.nan_to_num(), tiled.nan_to_num())
+    assert torch.equal(generic.isnan(), tiled.isnan())
+    err = ulp_errors(tiled.cpu().numpy(), O.student_map(z, nu, K, zstar), np.float64)
+    assert err.max() <= 2.0, summary(err)
+
+
 def test_student_default_crossover_is_the_papers():
     z = _z_inputs(np.float64)
     a = Q.qm_recycle_normal_to_t(torch.from_numpy(z).cuda(), 4.0, 10, 0.0)

@@ -1,0 +1,51 @@
+"""Time one hot-path call with CUDA events (A/B helper):  python tools/time_op.py <name> [reps]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_0901_0638_b200 as Q  # noqa: E402
+
+SEED = 0x5EEDC0FFEE123457
+name = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+if name == "fused_f32":
+    n = 1 << 32
+    z = torch.empty(n, dtype=torch.float32, device="cuda")
+    fn = lambda: Q.qm_normal_philox(n, SEED, 0, out=z)
+elif name.startswith("stream_f32"):
+    n = 1 << 28
+    alg = {"stream_f32": Q.BREAKLESS, "stream_f32_two": Q.TWO_REGION, "stream_f32_88": Q.BREAKLESS88}[name]
+    u = Q.qm_philox_uniform(n, SEED, 0)
+    z = torch.empty_like(u)
+    fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
+elif name == "stream_f64":
+    n = 1 << 28
+    u = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
+    z = torch.empty_like(u)
+    fn = lambda: Q.qm_normal_quantile(u, out=z)
+elif name == "fused_f64":
+    n = 1 << 31
+    z = torch.empty(n, dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_normal_philox(n, SEED, 0, dtype=torch.float64, out=z)
+elif name.startswith("student"):
+    n = 1 << 30
+    nu, K, zs = {"student4": (4.0, 10, 3.93473), "student5": (5.0, 16, 4.6506)}[name]
+    zn = Q.qm_normal_philox(n, SEED, 0, dtype=torch.float64)
+    t = torch.empty_like(zn)
+    fn = lambda: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=t)
+else:
+    raise SystemExit("unknown " + name)
+for _ in range(3):
+    fn()
+s = torch.cuda.current_stream()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+e0.record(s)
+for _ in range(reps):
+    fn()
+e1.record(s)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / reps
+print(f"{name} {os.environ.get('QM_PHILOX_CFG', '')}{os.environ.get('QM_TL_CFG', '')} {n / ms / 1e6:.1f} Gsamples/s ({ms:.3f} ms)")
