@@ -26,6 +26,20 @@ struct McParams {
     float K[QM_MC_MAXK];
 };
 
+// row columns 4q..4q+3 = (sum, sq) of strikes 2q and 2q+1, added into the
+// thread's fp64 accumulators
+QM_DEV void flush_pair(double *acc, int tid, int q, int nk, float2 sum, float2 sq)
+{
+    if (2 * q < nk) {
+        acc[(4 * q) * 256 + tid] = __dadd_rn(acc[(4 * q) * 256 + tid], (double)sum.x);
+        acc[(4 * q + 1) * 256 + tid] = __dadd_rn(acc[(4 * q + 1) * 256 + tid], (double)sq.x);
+    }
+    if (2 * q + 1 < nk) {
+        acc[(4 * q + 2) * 256 + tid] = __dadd_rn(acc[(4 * q + 2) * 256 + tid], (double)sum.y);
+        acc[(4 * q + 3) * 256 + tid] = __dadd_rn(acc[(4 * q + 3) * 256 + tid], (double)sq.y);
+    }
+}
+
 // NKMAX: register budget for the per-thread fp32 partials (instantiated for 8, 17, 32)
 template <int NKMAX>
 __global__ void __launch_bounds__(256)
@@ -39,10 +53,14 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
     const int64_t s0 = (int64_t)blockIdx.x * QM_MC_CHUNK;
     const int64_t s1 = (s0 + QM_MC_CHUNK < n) ? s0 + QM_MC_CHUNK : n;
     const int64_t b0 = s0 >> 2, b1 = (s1 + 3) >> 2;         // Philox blocks of this chunk
-    float part[2 * NKMAX];
-    int inpart = 0;
+    // per-thread fp32 partials: sum and sum of squares of each strike's payoff,
+    // strikes paired so that one FADD2 / FFMA2 updates two strikes (the same
+    // IEEE operations as one FADD / FFMA per strike: bitwise the same sums)
+    constexpr int NP = (NKMAX + 1) / 2;
+    float2 sum[NP], sq[NP];
 #pragma unroll
-    for (int j = 0; j < 2 * NKMAX; ++j) part[j] = 0.0f;
+    for (int q = 0; q < NP; ++q) { sum[q] = make_float2(0.0f, 0.0f); sq[q] = make_float2(0.0f, 0.0f); }
+    int inpart = 0;
 
     for (int64_t blk = b0 + tid; blk < b1; blk += 256) {
         const uint4 w = philox_block(c0 + (unsigned long long)blk, seed);
@@ -58,31 +76,35 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
             const int64_t i = 4 * blk + k;
             float z = rat32<ALG_BREAKLESS>(v[k]);
             z = ((ws[k] >> 8) & 1u) ? z : -z;
-            const float ST = expf(__fmaf_rn(mp.b, z, mp.a));
-            const bool in = i < s1;
+            // past the end of the chunk: S_T = -inf makes every payoff max(-inf, 0) = 0
+            const float ST = (i < s1) ? expf(__fmaf_rn(mp.b, z, mp.a)) : __int_as_float(0xff800000);
+            const float2 ST2 = make_float2(ST, ST);
 #pragma unroll
-            for (int j = 0; j < NKMAX; ++j) {
-                if (j < nk) {
-                    const float p = in ? fmaxf(__fsub_rn(ST, mp.K[j]), 0.0f) : 0.0f;
-                    part[2 * j] = __fadd_rn(part[2 * j], p);
-                    part[2 * j + 1] = __fmaf_rn(p, p, part[2 * j + 1]);
+            for (int q = 0; q < NP; ++q) {
+                if (2 * q + 1 < nk) {
+                    const float2 d = add2(ST2, make_float2(-mp.K[2 * q], -mp.K[2 * q + 1]));
+                    const float2 p = make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f));
+                    sum[q] = add2(sum[q], p);
+                    sq[q] = fma2(p, p, sq[q]);
+                } else if (2 * q < nk) {
+                    const float p = fmaxf(__fsub_rn(ST, mp.K[2 * q]), 0.0f);
+                    sum[q].x = __fadd_rn(sum[q].x, p);
+                    sq[q].x = __fmaf_rn(p, p, sq[q].x);
                 }
             }
         }
         if (++inpart == 16) {                   // 64 samples: flush into fp64
             inpart = 0;
 #pragma unroll
-            for (int j = 0; j < 2 * NKMAX; ++j) {
-                if (j < 2 * nk) {
-                    acc[j * 256 + tid] = __dadd_rn(acc[j * 256 + tid], (double)part[j]);
-                    part[j] = 0.0f;
-                }
+            for (int q = 0; q < NP; ++q) {
+                flush_pair(acc, tid, q, nk, sum[q], sq[q]);
+                sum[q] = make_float2(0.0f, 0.0f);
+                sq[q] = make_float2(0.0f, 0.0f);
             }
         }
     }
 #pragma unroll
-    for (int j = 0; j < 2 * NKMAX; ++j)
-        if (j < 2 * nk) acc[j * 256 + tid] = __dadd_rn(acc[j * 256 + tid], (double)part[j]);
+    for (int q = 0; q < NP; ++q) flush_pair(acc, tid, q, nk, sum[q], sq[q]);
     __syncthreads();
     // fixed tree over the 256 threads, column by column
     for (int w = 128; w > 0; w >>= 1) {

@@ -35,6 +35,12 @@ elif name.startswith("student"):
     zn = Q.qm_normal_philox(n, SEED, 0, dtype=torch.float64)
     t = torch.empty_like(zn)
     fn = lambda: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=t)
+elif name == "mc":
+    import numpy as np
+    n = 1 << 34
+    ks = list(np.linspace(50, 150, 17))
+    rows = torch.empty((Q.qm_mc_row_count(n), 34), dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_mc_european_call(n, SEED, 0, 100.0, 0.05, 0.2, 1.0, ks, out=rows)
 else:
     raise SystemExit("unknown " + name)
 for _ in range(3):
