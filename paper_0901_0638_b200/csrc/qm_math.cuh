@@ -328,6 +328,9 @@ enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5, ALG_F1212
 #define QM_TWO_BREAK_F32 10.0f
 #define QM_VC_F32 37.0f
 #define QM_VC_F64 86.75
+#ifndef QM_D13_KC
+#define QM_D13_KC 10     // compensated Horner steps of App D's 13 (A/B builds may override)
+#endif
 
 template <int ALG> __host__ __device__ constexpr int fast_alg()
 {
@@ -371,10 +374,10 @@ QM_DEV double rat64(dd z)
     if (ALG == ALG_F1212) return rational_dd<13, 12>(z, kF12P, kF12Q);
     if (ALG == ALG_F88) return rational_dd<9, 8>(z, kF88P_d, kF88Q_d);
     if (ALG == ALG_BREAKLESS_TAIL)
-        return (z.hi < QM_VC_F64) ? rational_dd<14, 10>(z, kD13P, kD13Q) : tail_model_q_dd(z);
+        return (z.hi < QM_VC_F64) ? rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q) : tail_model_q_dd(z);
     // compensating the last 10 of 13 Horner steps is enough: 0.65 ulp max over
     // 2^21 grid + tail-stratified inputs in emulation (all 13: 0.53; 9: 1.20)
-    return rational_dd<14, 10>(z, kD13P, kD13Q);
+    return rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
 }
 
 // fast path: requires vv = min(u, 1-u) >= 2^-126 (normal, not NaN)

@@ -2,7 +2,7 @@
 warp-instructions of each hot-path kernel (bench.py reads it for `roofline.traffic`
 and the issue-slot rooflines of the compute-bound rows).
 
-    python tools/ncu_facts.py profiles/r02
+    python tools/ncu_facts.py profiles/r01
 """
 import json
 import os
