@@ -71,23 +71,28 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
         const float2 v01 = neg_log2x_f32x2(u[0], u[1], -1);      // -log u
         const float2 v23 = neg_log2x_f32x2(u[2], u[3], -1);
         const float v[4] = {v01.x, v01.y, v23.x, v23.y};
+        // the four samples' chains (rational, exp) first, then the strikes: the
+        // per-strike sums still see the samples in the order k = 0..3
+        float ST[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int64_t i = 4 * blk + k;
             float z = rat32<ALG_BREAKLESS>(v[k]);
             z = ((ws[k] >> 8) & 1u) ? z : -z;
             // past the end of the chunk: S_T = -inf makes every payoff max(-inf, 0) = 0
-            const float ST = (i < s1) ? expf(__fmaf_rn(mp.b, z, mp.a)) : __int_as_float(0xff800000);
-            const float2 ST2 = make_float2(ST, ST);
+            ST[k] = (i < s1) ? expf(__fmaf_rn(mp.b, z, mp.a)) : __int_as_float(0xff800000);
+        }
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
+        for (int q = 0; q < NP; ++q) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
                 if (2 * q + 1 < nk) {
-                    const float2 d = add2(ST2, make_float2(-mp.K[2 * q], -mp.K[2 * q + 1]));
+                    const float2 d = add2(make_float2(ST[k], ST[k]), make_float2(-mp.K[2 * q], -mp.K[2 * q + 1]));
                     const float2 p = make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f));
                     sum[q] = add2(sum[q], p);
                     sq[q] = fma2(p, p, sq[q]);
                 } else if (2 * q < nk) {
-                    const float p = fmaxf(__fsub_rn(ST, mp.K[2 * q]), 0.0f);
+                    const float p = fmaxf(__fsub_rn(ST[k], mp.K[2 * q]), 0.0f);
                     sum[q].x = __fadd_rn(sum[q].x, p);
                     sq[q].x = __fmaf_rn(p, p, sq[q].x);
                 }
