@@ -41,7 +41,7 @@ QM_DEV void flush_pair(double *acc, int tid, int q, int nk, float2 sum, float2 s
 }
 
 // NKMAX: register budget for the per-thread fp32 partials (instantiated for 8, 17, 32)
-template <int NKMAX>
+template <int NKMAX, int VB = 1>
 __global__ void __launch_bounds__(256)
 k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __grid_constant__ McParams mp,
           double *__restrict__ rows)
@@ -62,21 +62,25 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
     for (int q = 0; q < NP; ++q) { sum[q] = make_float2(0.0f, 0.0f); sq[q] = make_float2(0.0f, 0.0f); }
     int inpart = 0;
 
-    for (int64_t blk = b0 + tid; blk < b1; blk += 256) {
-        const uint4 w = philox_block(c0 + (unsigned long long)blk, seed);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-        float u[4];
+    for (int64_t blk0 = b0 + tid; blk0 < b1; blk0 += 256 * VB) {
+        // VB Philox blocks (4 VB samples) per iteration: all chains first (ILP),
+        // then the strikes, which see the samples in stream order
+        float ST[4 * VB];
+        uint32_t ws[4 * VB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) u[k] = u01_f32(ws[k]);
-        const float2 v01 = neg_log2x_f32x2(u[0], u[1], -1);      // -log u
-        const float2 v23 = neg_log2x_f32x2(u[2], u[3], -1);
-        const float v[4] = {v01.x, v01.y, v23.x, v23.y};
-        // the four samples' chains (rational, exp) first, then the strikes: the
-        // per-strike sums still see the samples in the order k = 0..3
-        float ST[4];
+        for (int b = 0; b < VB; ++b) {
+            const uint4 w = philox_block(c0 + (unsigned long long)(blk0 + 256 * b), seed);
+            ws[4 * b] = w.x; ws[4 * b + 1] = w.y; ws[4 * b + 2] = w.z; ws[4 * b + 3] = w.w;
+        }
+        float v[4 * VB];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int64_t i = 4 * blk + k;
+        for (int k = 0; k < 4 * VB; k += 2) {
+            const float2 vv = neg_log2x_f32x2(u01_f32(ws[k]), u01_f32(ws[k + 1]), -1);   // -log u
+            v[k] = vv.x; v[k + 1] = vv.y;
+        }
+#pragma unroll
+        for (int k = 0; k < 4 * VB; ++k) {
+            const int64_t i = 4 * (blk0 + 256 * (k / 4)) + (k % 4);
             float z = rat32<ALG_BREAKLESS>(v[k]);
             z = ((ws[k] >> 8) & 1u) ? z : -z;
             // past the end of the chunk: S_T = -inf makes every payoff max(-inf, 0) = 0
@@ -85,7 +89,7 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < 4 * VB; ++k) {
                 if (2 * q + 1 < nk) {
                     const float2 d = add2(make_float2(ST[k], ST[k]), make_float2(-mp.K[2 * q], -mp.K[2 * q + 1]));
                     const float2 p = make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f));
@@ -98,7 +102,7 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
                 }
             }
         }
-        if (++inpart == 16) {                   // 64 samples: flush into fp64
+        if ((inpart += VB) == 16) {             // 64 samples: flush into fp64
             inpart = 0;
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
