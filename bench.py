@@ -268,7 +268,15 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     z1 = torch.empty_like(u1)
     for name, alg in [("breakless_D13", Q.BREAKLESS), ("as241", Q.AS241), ("acklam", Q.ACKLAM),
                       ("acklam_refined", Q.ACKLAM_REFINED), ("moro", Q.MORO), ("breakless77", Q.BREAKLESS77)]:
-        rec(f"config1_f64_2^20_{name}", lambda alg=alg: Q.qm_normal_quantile(u1, out=z1, alg=alg), 1 << 20, 16)
+        # ~25 us of work per launch: time a CUDA graph of 100 launches
+        graph = torch.cuda.CUDAGraph()
+        Q.qm_normal_quantile(u1, out=z1, alg=alg)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph):
+            for _ in range(100):
+                Q.qm_normal_quantile(u1, out=z1, alg=alg)
+        rec(f"config1_f64_2^20_{name}", graph.replay, 100 << 20, 16,
+            extra={"timing": "CUDA graph of 100 launches per step"})
     del u64, z64
     return out
 
