@@ -450,6 +450,31 @@ QM_DEV uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
     return c;
 }
 
+// the ten round keys of a seed, computed once per thread (loop-invariant; the
+// compiler otherwise re-derives them with UIADD3s inside the sample loops)
+struct PhiloxKeys {
+    uint32_t k0[10], k1[10];
+    QM_DEV explicit PhiloxKeys(unsigned long long seed)
+    {
+        uint32_t a = (uint32_t)seed, b = (uint32_t)(seed >> 32);
+#pragma unroll
+        for (int r = 0; r < 10; ++r) { k0[r] = a; k1[r] = b; a += 0x9E3779B9u; b += 0xBB67AE85u; }
+    }
+};
+
+QM_DEV uint4 philox_block(unsigned long long counter, const PhiloxKeys &K)
+{
+    uint4 c = make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t lo0, hi0, lo1, hi1;
+        mul_wide_u32(0xD2511F53u, c.x, lo0, hi0);
+        mul_wide_u32(0xCD9E8D57u, c.z, lo1, hi1);
+        c = make_uint4(hi1 ^ c.y ^ K.k0[r], lo1, hi0 ^ c.w ^ K.k1[r], lo0);
+    }
+    return c;
+}
+
 QM_DEV uint4 philox_block(unsigned long long counter, unsigned long long seed)
 {
     return philox4x32_10(make_uint4((uint32_t)counter, (uint32_t)(counter >> 32), 0u, 0u),

@@ -48,6 +48,7 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
 {
     extern __shared__ double acc[];            // [2 * nk][256]
     const int nk = mp.nk, tid = threadIdx.x;
+    const PhiloxKeys keys(seed);
     for (int j = 0; j < 2 * nk; ++j) acc[j * 256 + tid] = 0.0;
 
     const int64_t s0 = (int64_t)blockIdx.x * QM_MC_CHUNK;
@@ -69,7 +70,7 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
         uint32_t ws[4 * VB];
 #pragma unroll
         for (int b = 0; b < VB; ++b) {
-            const uint4 w = philox_block(c0 + (unsigned long long)(blk0 + 256 * b), seed);
+            const uint4 w = philox_block(c0 + (unsigned long long)(blk0 + 256 * b), keys);
             ws[4 * b] = w.x; ws[4 * b + 1] = w.y; ws[4 * b + 2] = w.z; ws[4 * b + 3] = w.w;
         }
         float v[4 * VB];
