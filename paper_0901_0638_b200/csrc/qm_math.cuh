@@ -294,12 +294,47 @@ QM_DEV dd horner_comp(const double *a, double zh, double zl)
     return dd{s, c};
 }
 
-// z P(z)/Q(z) for a double-double z >= 0, one final rounding
+// The same compensated Horner for POSITIVE coefficients and zh >= 0 (every
+// breakless rational: all its coefficients are positive).  Then p = s zh >= 0
+// and a_i > 0, so the sum's error is exact with Fast2Sum once the larger
+// operand is first; for positive doubles the order of the high words decides it
+// (equal high words: equal exponents, either order is exact).  The compare and
+// selects run on the integer pipe: 3 DADD + ISETP + 4 SEL per step instead of
+// TwoSum's 6 DADD on the FP64 pipe -- bitwise the same result (both errors exact).
+QM_DEV dd two_sum_pos(double p, double a)
+{
+    const bool pa = __double2hiint(p) >= __double2hiint(a);
+    const double hi = pa ? p : a, lo = pa ? a : p;
+    const double t = __dadd_rn(hi, lo);
+    return dd{t, __dadd_rn(lo, -__dadd_rn(t, -hi))};
+}
+
+template <int N, int KC>
+QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
+{
+    double s = a[N - 1], c = 0.0;
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {
+        if (i >= KC) {
+            s = __fma_rn(s, zh, a[i]);
+        } else {
+            const double p = __dmul_rn(s, zh);
+            const double pi = __fma_rn(s, zh, -p);               // TwoProd
+            const dd t = two_sum_pos(p, a[i]);                   // Fast2Sum, ordered
+            c = __fma_rn(c, zh, __fma_rn(s, zl, __dadd_rn(pi, t.lo)));
+            s = t.hi;
+        }
+    }
+    return dd{s, c};
+}
+
+// z P(z)/Q(z) for a double-double z >= 0, one final rounding (positive
+// coefficients: the breakless rationals)
 template <int N, int KC>
 QM_DEV double rational_dd(dd z, const double *P, const double *Q)
 {
-    const dd p = horner_comp<N, KC>(P, z.hi, z.lo);
-    const dd q = horner_comp<N, KC>(Q, z.hi, z.lo);
+    const dd p = horner_comp_pos<N, KC>(P, z.hi, z.lo);
+    const dd q = horner_comp_pos<N, KC>(Q, z.hi, z.lo);
     double r = rcp_approx_f64(q.hi);
     r = __fma_rn(r, __fma_rn(-q.hi, r, 1.0), r);
     const double q0 = __dmul_rn(p.hi, r);
