@@ -309,6 +309,17 @@ QM_DEV dd two_sum_pos(double p, double a)
     return dd{t, __dadd_rn(lo, -__dadd_rn(t, -hi))};
 }
 
+// Fast2Sum with the operands ordered by magnitude (any signs): |x| >= |y| is
+// decided on the high words with the sign masked (equal high words: equal
+// exponents, exact either way).  Exact like TwoSum, 3 DADD instead of 6.
+QM_DEV dd two_sum_ord(double p, double a)
+{
+    const bool pa = (__double2hiint(p) & 0x7fffffff) >= (__double2hiint(a) & 0x7fffffff);
+    const double hi = pa ? p : a, lo = pa ? a : p;
+    const double t = __dadd_rn(hi, lo);
+    return dd{t, __dadd_rn(lo, -__dadd_rn(t, -hi))};
+}
+
 template <int N, int KC>
 QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 {

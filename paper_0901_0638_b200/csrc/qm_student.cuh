@@ -55,11 +55,9 @@ QM_DEV double student_central_k(const StudentParams &sp, double a)
         } else {
             const double p = __dmul_rn(s, yh);
             const double pi = __fma_rn(s, yh, -p);
-            const double t = __dadd_rn(p, sp.c[i]);
-            const double bb = __dadd_rn(t, -p);
-            const double sg = __dadd_rn(__dadd_rn(p, -__dadd_rn(t, -bb)), __dadd_rn(sp.c[i], -bb));
-            c = __fma_rn(c, yh, __fma_rn(s, yl, __dadd_rn(pi, sg)));
-            s = t;
+            const dd t = two_sum_ord(p, sp.c[i]);            // = TwoSum, bitwise
+            c = __fma_rn(c, yh, __fma_rn(s, yl, __dadd_rn(pi, t.lo)));
+            s = t.hi;
         }
     }
     return __fma_rn(a, s, __dmul_rn(a, c));
