@@ -328,6 +328,42 @@ k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, in
         z[j] = nq_f64_careful<ALG>(u[j]);
 }
 
+// fp64 map through the TMA-in / streaming-store pipeline: a lane's slice of PER
+// double2 under one vote per double2 (64 samples per warp vote)
+template <int ALG>
+struct MapNormalF64 {
+    template <int PER>
+    QM_DEV void map_slice(double2 *a) const
+    {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const double x0 = a[j].x, x1 = a[j].y;
+            const bool ok = (fmin(x0, __dadd_rn(1.0, -x0)) >= fast_vv_min_f64<ALG>()) &
+                            (fmin(x1, __dadd_rn(1.0, -x1)) >= fast_vv_min_f64<ALG>());
+            if (__all_sync(0xffffffffu, ok)) a[j] = make_double2(nq_f64_fast<ALG>(x0), nq_f64_fast<ALG>(x1));
+            else a[j] = make_double2(nq_f64_careful<ALG>(x0), nq_f64_careful<ALG>(x1));
+        }
+    }
+};
+
+// 1 CTA/SM: producer + NC consumer warps, 4 stages of TILE_VECS double2
+template <int NC_, int TILE_VECS_>
+struct TlCfgF64 {
+    static constexpr int NC = NC_, STAGES = 4, TILE_VECS = TILE_VECS_, THREADS = 32 * (NC_ + 1);
+    static constexpr int TILE = 2 * TILE_VECS_;                          // doubles per tile
+};
+using TlF64A = TlCfgF64<12, 1536>;    // 13 warps, 4 x 24 KB, 4 double2 per lane
+using TlF64B = TlCfgF64<16, 2048>;    // 17 warps, 4 x 32 KB, 4 double2 per lane
+
+template <int ALG, class CFG>
+__global__ void __launch_bounds__(CFG::THREADS, 1)
+k_normal_f64_tl(const double *__restrict__ u, double *__restrict__ z, int64_t ntiles)
+{
+    tma_load_map<double2, CFG::TILE_VECS, CFG::STAGES, CFG::NC>(reinterpret_cast<const double2 *>(u),
+                                                               reinterpret_cast<double2 *>(z), ntiles,
+                                                               MapNormalF64<ALG>{});
+}
+
 // --------------------------------------------------- Philox uniforms / fused
 // MODE 0: write the uniforms; MODE 1: write the normal quantile of them (fused).
 template <int MODE, int ALG, int V = 2, int MINB = 1>   // V: Philox blocks per lane per chunk

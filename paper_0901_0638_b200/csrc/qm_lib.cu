@@ -239,6 +239,31 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     default: break;
     }
     const int g = grid_for(n, kThreads * 2, 8);
+    if (alg == QM_BREAKLESS && vec && stream_path() == 2) {
+        static int cfg = -1;   // QM_TL64_CFG (A/B): 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B
+        if (cfg < 0) { const char *e = getenv("QM_TL64_CFG"); cfg = e ? atoi(e) : 1; }
+        if (cfg > 0) {
+            auto go = [&](auto k, int tile, int threads, size_t smem) {
+                const int64_t ntiles = n / tile;
+                if (ntiles > 0) {
+                    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                        return QM_ECUDA;
+                    const int sms = sm_count_for_current_device();
+                    const int64_t gg = ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148);
+                    k<<<(int)gg, threads, smem, s>>>(ud, zd, ntiles);
+                }
+                const int64_t done = ntiles * tile;
+                if (n > done)
+                    k_normal_f64<ALG_BREAKLESS><<<grid_for(n - done, kThreads * 2, 8), kThreads, 0, s>>>(ud + done, zd + done,
+                                                                                                n - done, 1);
+                return launched();
+            };
+            if (cfg == 2) return go(k_normal_f64_tl<ALG_BREAKLESS, TlF64B>, TlF64B::TILE, TlF64B::THREADS,
+                                    (size_t)TlF64B::STAGES * TlF64B::TILE_VECS * 16);
+            return go(k_normal_f64_tl<ALG_BREAKLESS, TlF64A>, TlF64A::TILE, TlF64A::THREADS,
+                      (size_t)TlF64A::STAGES * TlF64A::TILE_VECS * 16);
+        }
+    }
     return with_breakless(alg, [&](auto A) {
         k_normal_f64<decltype(A)::value><<<g, kThreads, 0, s>>>(ud, zd, n, vec);
         return launched();
