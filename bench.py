@@ -278,7 +278,42 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
         rec(f"config1_f64_2^20_{name}", graph.replay, 100 << 20, 16,
             extra={"timing": "CUDA graph of 100 launches per step"})
     del u64, z64
+    out["size_sweep"] = size_sweep(Q, torch)
     return out
+
+
+def size_sweep(Q, torch):
+    """Gsamples/s over 2^20 .. 2^34 samples (north star), 1 GPU: the fp32 streaming
+    map (inputs resident in HBM) and the Philox-fused fp32 sampler.  Sizes whose
+    launch is shorter than ~1 ms are timed as CUDA graphs of 50 launches."""
+    res = {"stream_f32": {}, "fused_f32": {}}
+
+    def timed(fn, n, tag):
+        one = time_steps(fn, 3, 2) / 3
+        if one < 1.0:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(50):
+                    fn()
+            ms = time_steps(g.replay, 5, 2) / (5 * 50)
+        else:
+            ms = time_steps(fn, 5, 2) / 5
+        res[tag][f"2^{n.bit_length() - 1}"] = round(n / (ms / 1e3) / 1e9, 2)
+
+    for e in (20, 22, 24, 26, 28, 30, 32):
+        n = 1 << e
+        u = torch.empty(n, dtype=torch.float32, device="cuda")
+        Q.qm_philox_uniform(n, SEED, 0, out=u)
+        z = torch.empty_like(u)
+        timed(lambda: Q.qm_normal_quantile(u, out=z), n, "stream_f32")
+        del u, z
+    for e in (20, 24, 28, 32, 34):
+        n = 1 << e
+        z = torch.empty(n, dtype=torch.float32, device="cuda")
+        timed(lambda: Q.qm_normal_philox(n, SEED, 0, out=z), n, "fused_f32")
+        del z
+    torch.cuda.empty_cache()
+    return res
 
 
 def dist_variants(torch, dist, rank, world, steps=5, warmup=2):

@@ -89,7 +89,9 @@ template <class CFG, typename KT, typename KL>
 qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64_t n, cudaStream_t s)
 {
     const int vec = aligned16(in) && aligned16(out);
-    int64_t ntiles = (vec && tma_enabled()) ? n / CFG::TILE : 0;
+    // below 2^23 samples the LDG kernel balances better (measured: 2^20 273 vs 262,
+    // 2^22 454 vs 442 Gsamples/s; from 2^23 the pipeline wins, 569 vs 491)
+    int64_t ntiles = (vec && tma_enabled() && n >= ((int64_t)1 << 23)) ? n / CFG::TILE : 0;
     if (ntiles > 0) {
         const size_t smem = (size_t)CFG::STAGES * CFG::TILE * sizeof(float);
         if (cudaFuncSetAttribute(ktma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -239,7 +241,9 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     default: break;
     }
     const int g = grid_for(n, kThreads * 2, 8);
-    if (alg == QM_BREAKLESS && vec && stream_path() == 2) {
+    // the pipeline only pays with several tiles per CTA (small n: the LDG kernel
+    // balances better, e.g. config 1's 2^20: 55 vs 40 Gsamples/s)
+    if (alg == QM_BREAKLESS && vec && stream_path() == 2 && n >= ((int64_t)1 << 23)) {
         static int cfg = -1;   // QM_TL64_CFG (A/B): 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B
         if (cfg < 0) { const char *e = getenv("QM_TL64_CFG"); cfg = e ? atoi(e) : 1; }
         if (cfg > 0) {

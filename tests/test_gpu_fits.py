@@ -31,9 +31,10 @@ def _deep(dtype, n=20000, seed=7):
     return np.concatenate([t, 1 - t[: n // 10]]).astype(dtype)
 
 
+@pytest.mark.parametrize("n", [(1 << 20) + 37, (1 << 23) + 37])
 @pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
-def test_single_patch_fits(dtype, alg, formula, prec, bar):
-    u = np.concatenate([I.mixed_uniforms((1 << 20) + 37, dtype=dtype), _deep(dtype)])
+def test_single_patch_fits(dtype, alg, formula, prec, bar, n):
+    u = np.concatenate([I.mixed_uniforms(n, dtype=dtype), _deep(dtype)])
     g = _gpu(u, alg)
     err = ulp_errors(g, O.normal_breakless(u.astype(np.float64), formula, prec), dtype)
     assert err.max() <= bar, summary(err)
@@ -61,8 +62,9 @@ def _two_region_ref(u):
     return ref, alt, near
 
 
-def test_two_region_fp32():
-    u = np.concatenate([I.mixed_uniforms((1 << 20) + 37, dtype=np.float32), _deep(np.float32),
+@pytest.mark.parametrize("n", [(1 << 20) + 37, (1 << 23) + 37])
+def test_two_region_fp32(n):
+    u = np.concatenate([I.mixed_uniforms(n, dtype=np.float32), _deep(np.float32),
                         (np.exp(-10.0) / 2 * (1 + np.linspace(-1e-4, 1e-4, 2001))).astype(np.float32)])
     g = _gpu(u, Q.TWO_REGION)
     ref, alt, near = _two_region_ref(u)

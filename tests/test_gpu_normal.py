@@ -28,11 +28,13 @@ def _gpu(fn, x_np, **kw):
     return fn(x, **kw).cpu().numpy()
 
 
+@pytest.mark.parametrize("n", [(1 << 20) + 37, (1 << 23) + 37])
 @pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
-def test_normal_quantile_mixed_inputs(dtype, alg, formula, prec, bar):
-    """2^20 + 37 inputs: odd-grid uniforms, log-uniform tails, edge values (0, 1, 1/2,
-    subnormals, NaN, out of range); several chunks of every warp and a ragged tail."""
-    u = I.mixed_uniforms((1 << 20) + 37, dtype=dtype)
+def test_normal_quantile_mixed_inputs(dtype, alg, formula, prec, bar, n):
+    """Odd-grid uniforms, log-uniform tails, edge values (0, 1, 1/2, subnormals, NaN,
+    out of range); several chunks of every warp and a ragged tail.  2^20 + 37 runs
+    the LDG kernels, 2^23 + 37 the TMA pipelines (whole tiles) plus the remainder."""
+    u = I.mixed_uniforms(n, dtype=dtype)
     g = _gpu(Q.qm_normal_quantile, u, alg=alg)
     ref = O.normal_breakless(u.astype(np.float64), formula, prec)
     err = ulp_errors(g, ref, dtype)

@@ -15,18 +15,19 @@ Q = pytest.importorskip("paper_0901_0638_b200")
 VC = {np.float32: (O.C55, 32, 37.0, 4.0), np.float64: (O.D13, 64, 86.75, 2.0)}
 
 
-def _deep_uniforms(dtype):
+def _deep_uniforms(dtype, nmix=20000):
     rng = np.random.default_rng(11)
     lo = -44 if dtype == np.float32 else -320
     t = 10.0 ** rng.uniform(lo, -15, 20000)                 # v = -log(2t) from ~33 up to the range end
-    u = np.concatenate([t, 1 - t[:100], I.mixed_uniforms(20000, dtype=dtype).astype(np.float64)])
+    u = np.concatenate([t, 1 - t[:100], I.mixed_uniforms(nmix, dtype=dtype).astype(np.float64)])
     return u.astype(dtype)
 
 
+@pytest.mark.parametrize("nmix", [20000, 1 << 23])          # LDG kernels / TMA pipelines
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_tail_composite_quantile(dtype):
+def test_tail_composite_quantile(dtype, nmix):
     f, p, vc, bar = VC[dtype]
-    u = _deep_uniforms(dtype)
+    u = _deep_uniforms(dtype, nmix)
     g = Q.qm_normal_quantile(torch.from_numpy(u).cuda(), alg=Q.BREAKLESS_TAIL).cpu().numpy()
     ref = O.normal_breakless_tail(u.astype(np.float64), f, p, vc)
     err = ulp_errors(g, ref, dtype)
