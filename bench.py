@@ -136,6 +136,17 @@ def oracle_rate(n_sample, threads, seed=SEED, chunk=None):
     return n_sample / dt / 1e9, dt
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args):
     world, rank, _ = dist_setup(args.gpus)
     if rank != 0:
@@ -157,7 +168,7 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": WORKLOAD, "n": N_MAIN, "reference_sample_per_step": n_step},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{n_step} fp32 odd-grid uniforms per step -> same formula (App C, "
                                        f"float-rounded coefficients) in long double, {threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -256,6 +267,18 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     zo = torch.empty_like(v)
     rec("exp_to_normal_f32_2^28", lambda: Q.qm_recycle_exp_to_normal(v, out=zo), n, 8)
     del v, zo
+    # row f1: exponential base -> hyperbolic / VG through the RODE table (fp64 and fp32)
+    tab_h = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+    tab_v = Q.qm_exp_target_table(Q.VG, [2.0, 1.0, 0.5])
+    v64 = torch.from_numpy(I.laplace(n, dtype=np.float64)).cuda()
+    x64 = torch.empty_like(v64)
+    rec("exp_to_hyperbolic_f64_2^28", lambda: Q.qm_recycle_exp_to_hyperbolic(v64, tab_h, out=x64), n, 16)
+    rec("exp_to_vg_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_v, out=x64), n, 16)
+    del v64, x64
+    xf = torch.empty(n, dtype=torch.float32, device="cuda")
+    rec("hyperbolic_philox_f32_2^28", lambda: Q.qm_exp_target_philox(n, tab_h, SEED, 0, dtype=torch.float32, out=xf),
+        n, 4)
+    del xf
     # config 5: 2^34-sample exponential-base Monte-Carlo call sweep, 17 strikes (Philox-fused)
     strikes = list(np.linspace(50, 150, 17))
     rows = torch.empty((Q.qm_mc_row_count(1 << 34), 34), dtype=torch.float64, device="cuda")
@@ -403,10 +426,13 @@ def run_ours(args):
         # bounded sample sized for ~10-30 s of CPU work (the oracle runs ~20 M samples/s/thread)
         nsamp = 1 << 28 if threads >= 8 else 1 << 26
         rate, dt = oracle_rate(nsamp, threads)
+        rate1, dt1 = oracle_rate(1 << 24, 1)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"2^{nsamp.bit_length() - 1} fp32 odd-grid uniforms (the full configs[1] batch when "
                          f"2^28) -> the same formula (App C, float-rounded coefficients) in long double, "
-                         f"{dt:.1f} s wall on {threads} threads"}
+                         f"{dt:.1f} s wall on {threads} threads",
+               "single_thread_value": rate1, "single_thread_sample": f"2^24 samples, {dt1:.1f} s",
+               "cpu_model": cpu_model()}
 
     # configs 4 and 5 across the ranks: fixed global work split by Philox counter
     # ranges, one NCCL all-reduce of the fixed-chunk sum rows (strong scaling)

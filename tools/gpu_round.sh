@@ -16,9 +16,15 @@ for k in ${PROFS:-}; do
   case $k in
     stream_f32) prof stream_f32 k_normal_f32_tl; cp /tmp/prof_stream_f32.ncu-rep gpurun_out/ ;;
     fused_f32) prof fused_f32 k_philox_f32 ;;
-    student) prof student k_student_f64_tl ;;
     mc) prof mc k_mc_call ;;
     config1_moro) prof config1_moro k_branchy ;;
+    stream_f64) prof stream_f64 k_normal_f64_tl ;;
+    fused_f64) prof fused_f64 k_philox_f64 ;;
+    student) prof student k_student_f64_tl ;;
+    exp2n_f32) prof exp2n_f32 k_exp2n_f32_tl ;;
+    rode_hyp_f64) prof rode_hyp_f64 k_rode_map ;;
+    rode_philox_f32) prof rode_philox_f32 k_rode_philox ;;
+    two_region) prof two_region k_normal_f32_tl "" stream_f32_two ;;
   esac
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/launches.csv \

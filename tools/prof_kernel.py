@@ -11,10 +11,11 @@ SEED = 0x5EEDC0FFEE123457
 name = sys.argv[1] if len(sys.argv) > 1 else "stream_f32"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 n = 1 << 28
-if name == "stream_f32":
+if name in ("stream_f32", "stream_f32_two"):
     u = Q.qm_philox_uniform(n, SEED, 0)
     z = torch.empty_like(u)
-    fn = lambda: Q.qm_normal_quantile(u, out=z)
+    alg = Q.TWO_REGION if name == "stream_f32_two" else Q.BREAKLESS
+    fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
 elif name == "stream_f64":
     u = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
     z = torch.empty_like(u)
@@ -52,6 +53,17 @@ elif name == "student":
     zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
     t = torch.empty_like(zn)
     fn = lambda: Q.qm_recycle_normal_to_t(zn, 4.0, 10, 3.93473, out=t)
+elif name in ("rode_hyp_f64", "rode_philox_f32"):
+    import numpy as np
+    from synth import inputs as I
+    tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+    if name == "rode_hyp_f64":
+        v = torch.from_numpy(I.laplace(n, dtype=np.float64)).cuda()
+        x = torch.empty_like(v)
+        fn = lambda: Q.qm_recycle_exp_to_hyperbolic(v, tab, out=x)
+    else:
+        x = torch.empty(n, dtype=torch.float32, device="cuda")
+        fn = lambda: Q.qm_exp_target_philox(n, tab, SEED, 0, dtype=torch.float32, out=x)
 else:
     raise SystemExit(f"unknown {name}")
 for _ in range(reps):
