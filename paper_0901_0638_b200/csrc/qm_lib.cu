@@ -416,10 +416,39 @@ static qm_status rode_map_launch(const void *v, void *x, int64_t n, qm_precision
     if (n < 0 || bad_ptrs(v, x, n) || tab == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const int g = grid_for(n, kThreads, 8);
-    if (p == QM_F64) k_rode_map<double><<<g, kThreads, 0, s>>>((const double *)v, (double *)x, n, tab);
-    else k_rode_map<float><<<g, kThreads, 0, s>>>((const float *)v, (float *)x, n, tab);
-    return launched();
+    // large aligned arrays: whole tiles through the TMA pipeline, the rest below
+    int64_t done = 0;
+    if (aligned16(v) && aligned16(x) && n >= ((int64_t)1 << 23)) {
+        const int64_t tile = (int64_t)kRodeTlTileVecs * (p == QM_F64 ? 2 : 4);
+        const int64_t ntiles = n / tile;
+        const int sms = sm_count_for_current_device();
+        const int gg = (int)(ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148));
+        auto tl = [&](auto k, auto *vv, auto *xx) {
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRodeTlSmemBytes) != cudaSuccess)
+                return QM_ECUDA;
+            k<<<gg, 32 * (kRodeTlNC + 1), kRodeTlSmemBytes, s>>>(vv, xx, ntiles, tab);
+            return QM_OK;
+        };
+        const qm_status r = (p == QM_F64) ? tl(k_rode_map_tl<double2>, (const double2 *)v, (double2 *)x)
+                                          : tl(k_rode_map_tl<float4>, (const float4 *)v, (float4 *)x);
+        if (r != QM_OK) return r;
+        done = ntiles * tile;
+        if (done == n) return launched();
+        const size_t es = (p == QM_F64) ? 8 : 4;
+        v = (const char *)v + done * es;
+        x = (char *)x + done * es;
+        n -= done;
+    }
+    // persistent: one 512-thread CTA per SM, each staging the centre nodes (197 KB)
+    const int g = grid_for(n, 512 * 4, 1);
+    auto go = [&](auto k, auto *vv, auto *xx) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRodeSmemBytes) != cudaSuccess)
+            return QM_ECUDA;
+        k<<<g, 512, kRodeSmemBytes, s>>>(vv, xx, n, tab);
+        return launched();
+    };
+    if (p == QM_F64) return go(k_rode_map<double>, (const double *)v, (double *)x);
+    return go(k_rode_map<float>, (const float *)v, (float *)x);
 }
 
 qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p, const double *table_dev,
@@ -452,13 +481,14 @@ qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double 
     if (n < 0 || (n > 0 && x == nullptr) || table_dev == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if (p == QM_F64)
-        k_rode_philox<double><<<grid_for((n + 1) / 2, kThreads, 8), kThreads, 0, s>>>((double *)x, n, seed,
-                                                                                       counter_offset, table_dev);
-    else
-        k_rode_philox<float><<<grid_for((n + 3) / 4, kThreads, 8), kThreads, 0, s>>>((float *)x, n, seed,
-                                                                                      counter_offset, table_dev);
-    return launched();
+    auto go = [&](auto k, auto *xx, int64_t nb) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRodeSmemBytes) != cudaSuccess)
+            return QM_ECUDA;
+        k<<<grid_for(nb, 512 * 2, 1), 512, kRodeSmemBytes, s>>>(xx, n, seed, counter_offset, table_dev);
+        return launched();
+    };
+    if (p == QM_F64) return go(k_rode_philox<double>, (double *)x, (n + 1) / 2);
+    return go(k_rode_philox<float>, (float *)x, (n + 3) / 4);
 }
 
 int64_t qm_mc_row_count(int64_t n) { return n > 0 ? (n + QM_MC_CHUNK - 1) / QM_MC_CHUNK : 0; }
@@ -486,7 +516,7 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
         return launched();
     };
     if (nk <= 8) return go(k_mc_call<8>);
-    if (nk <= 17) return go(k_mc_call<17>);
+    if (nk <= 17) return go(k_mc_call<17, 1, 3>);
     return go(k_mc_call<32>);
 }
 

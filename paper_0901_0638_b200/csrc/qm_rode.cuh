@@ -14,55 +14,184 @@
 #pragma once
 #include "qm_dd.cuh"
 #include "qm_rode_params.h"
+#include "qm_tma.cuh"
 
 namespace qm {
 
-QM_DEV double rode_eval(const double *__restrict__ tab, double v)
+// Centre-segment nodes staged in shared memory: (R, R', R'') per node, 3 doubles,
+// nodes 0..Nc of both sides (2 x 4097 x 24 B = 197 KB).  The centre covers
+// rate |v| <= 2, i.e. 1 - e^-2 = 86 % of the base samples; the other nodes are
+// gathered from the table in global memory (L2-resident).
+constexpr int kRodeSmemNodes = QM_RODE_CENTRE_NODES + 1;
+constexpr size_t kRodeSmemBytes = (size_t)(QM_RODE_HEADER + 2 * kRodeSmemNodes * 3) * sizeof(double);
+// with the TMA input pipeline (3 x 16 KB of stages) only nodes 0..3599 of each
+// side fit (173 KB): rate |v| <= 1.76, 83 % of the samples
+#ifndef QM_RODE_TL_NODES
+#define QM_RODE_TL_NODES 3600
+#endif
+constexpr int kRodeTlNodes = QM_RODE_TL_NODES;
+constexpr int kRodeTlStages = 3, kRodeTlTileVecs = 1024, kRodeTlNC = 16;
+constexpr size_t kRodeTlTileBytes = (size_t)kRodeTlStages * kRodeTlTileVecs * 16;
+constexpr size_t kRodeTlSmemBytes = kRodeTlTileBytes + (size_t)(QM_RODE_HEADER + 2 * kRodeTlNodes * 3) * sizeof(double);
+
+// shared-memory layout: the table header (segment records, Vmax; 80 doubles)
+// then (R, R', R'') of nodes 0..M-1 of side 0, then of side 1
+constexpr int kRodeSmHdr = QM_RODE_HEADER;
+
+template <int M = kRodeSmemNodes>
+QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
+{
+    for (int i = threadIdx.x; i < kRodeSmHdr; i += blockDim.x) sm[i] = __ldg(tab + i);
+    for (int i = threadIdx.x; i < 2 * M; i += blockDim.x) {
+        const int side = i / (M > 0 ? M : 1), k = i - side * M;
+        const double *g = tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
+        double *d = sm + kRodeSmHdr + 3 * i;
+        d[0] = __ldg(g); d[1] = __ldg(g + 1); d[2] = __ldg(g + 2);
+    }
+    __syncthreads();
+}
+
+// one sample split in three phases so that a batch of samples has all its node
+// gathers in flight together (the map is latency-bound on them: with 83-86 % of
+// the nodes in shared memory almost every warp still has a lane in L2)
+struct RodePrep {
+    const double *b;     // node k of the sample's side (shared or global memory)
+    int st;              // doubles from node k to node k+1 (3 shared, 4 global)
+    double t, h, a, vmax;
+};
+
+template <int M>
+QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double *sm)
 {
     const int side = (v < 0.0) ? 1 : 0;
     const double a = fabs(v);
-    const double *sg = tab + QM_RODE_SEG + 24 * side;          // 3 segment records of 8 doubles
-    const double Vmax = __ldg(tab + 28 + side);
-    const double2 *nd = reinterpret_cast<const double2 *>(tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1));
+    const double *sg = sm + QM_RODE_SEG + 24 * side;            // 3 segment records of 8 doubles
+    const double vmax = sm[28 + side];
     // segment j = [a >= Wc] + [a >= V] (selects; NaN lands in j = 0 and is replaced later)
-    const int j = (a >= __ldg(sg + 8)) + (a >= __ldg(sg + 16));
-    const double2 r01 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j));       // w0, h
-    const double2 r23 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j + 2));   // 1/h, k0
-    const double2 r45 = __ldg(reinterpret_cast<const double2 *>(sg + 8 * j + 4));   // n, w1
-    const double h = r01.y;
-    const double s = fmin((a - r01.x) * r23.x, r45.x);        // local coordinate in [0, n]
-    const double fk = fmin(floor(s), r45.x - 1.0);
-    const int k = (int)r23.y + (int)fk;
-    const double t = s - fk;
-    // node k: (R, R') at nd[2k], (R'', 0) at nd[2k+1]
-    const double2 n0 = __ldg(nd + 2 * k), c0 = __ldg(nd + 2 * k + 1);
-    const double2 n1 = __ldg(nd + 2 * k + 2), c1 = __ldg(nd + 2 * k + 3);
-    // quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
-    const double m0 = h * n0.y, m1 = h * n1.y, h2 = h * h;
-    const double a0 = h2 * c0.x, a1 = h2 * c1.x, dp = n1.x - n0.x;
+    const int j = (a >= sg[8]) + (a >= sg[16]);
+    const double *r = sg + 8 * j;                               // w0, h, 1/h, k0, n, w1
+    const double s = fmin((a - r[0]) * r[2], r[4]);             // local coordinate in [0, n]
+    const double fk = fmin(floor(s), r[4] - 1.0);
+    const int k = (int)r[3] + (int)fk;
+    const bool in_sm = (M > 0) && (j == 0) && (k + 1 < M);
+    RodePrep p;
+    p.b = in_sm ? sm + kRodeSmHdr + 3 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
+    p.st = in_sm ? 3 : 4;
+    p.t = s - fk;
+    p.h = r[1];
+    p.a = a;
+    p.vmax = vmax;
+    return p;
+}
+
+struct RodeNodes { double r0, d0, dd0, r1, d1, dd1; };
+
+template <int M>
+QM_DEV RodeNodes rode_load(const RodePrep &p)
+{
+    if constexpr (M == 0) {   // every node from global memory (L1-cached 16-byte gathers)
+        const double2 n0 = __ldg(reinterpret_cast<const double2 *>(p.b));
+        const double2 n1 = __ldg(reinterpret_cast<const double2 *>(p.b + 4));
+        return RodeNodes{n0.x, n0.y, __ldg(p.b + 2), n1.x, n1.y, __ldg(p.b + 6)};
+    } else {
+        return RodeNodes{p.b[0], p.b[1], p.b[2], p.b[p.st], p.b[p.st + 1], p.b[p.st + 2]};
+    }
+}
+
+// quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
+QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
+{
+    const double h = p.h, t = p.t;
+    const double m0 = h * n.d0, m1 = h * n.d1, h2 = h * h;
+    const double a0 = h2 * n.dd0, a1 = h2 * n.dd1, dp = n.r1 - n.r0;
     const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
     const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
     const double c5 = 6.0 * dp - 3.0 * m0 - 3.0 * m1 - 0.5 * a0 + 0.5 * a1;
-    const double q = n0.x + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
-    const double qx = n1.x + (a - Vmax) * n1.y;              // beyond Vmax: n1 = node NT
-    return (a <= Vmax) ? q : qx;
+    const double q = n.r0 + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
+    const double qx = n.r1 + (p.a - p.vmax) * n.d1;             // beyond Vmax: node k+1 = node NT
+    return (p.a <= p.vmax) ? q : qx;
 }
 
-// x = Q(v) with IEEE semantics: +-0 -> +-0, +-inf -> +-inf, NaN -> NaN
-QM_DEV double rode_map(const double *__restrict__ tab, double v)
+// IEEE semantics of the map: +-0 -> +-0, +-inf -> +-inf, NaN -> NaN
+QM_DEV double rode_special(double v, double q)
 {
-    const double q = rode_eval(tab, v);
     const double r = (v == 0.0) ? v : q;
     return (fabs(v) < __longlong_as_double(0x7ff0000000000000LL)) ? r : v;
 }
 
+// B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
+// issued before their arithmetic (4 keeps the state in registers)
+template <int M, int B>
+QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const double (&v)[B], double (&x)[B])
+{
+    constexpr int G = B < 4 ? B : 4;
+    static_assert(B % G == 0, "batch must split into groups of 4");
+#pragma unroll
+    for (int g = 0; g < B; g += G) {
+        RodePrep p[G];
+        RodeNodes nd[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) p[k] = rode_prep<M>(tab, v[g + k], sm);
+#pragma unroll
+        for (int k = 0; k < G; ++k) nd[k] = rode_load<M>(p[k]);
+#pragma unroll
+        for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_finish(p[k], nd[k]));
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512, 1)
 k_rode_map(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *__restrict__ tab)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        x[i] = (T)rode_map(tab, (double)v[i]);
+    extern __shared__ __align__(16) double rode_sm[];
+    rode_stage_centre(tab, rode_sm);
+    constexpr int U = 4;
+    const int64_t S = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * S) {
+        double a[U], r[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) a[k] = (i0 + k * S < n) ? (double)v[i0 + k * S] : 0.0;
+        rode_map_batch<kRodeSmemNodes, U>(tab, rode_sm, a, r);
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i0 + k * S < n) x[i0 + k * S] = (T)r[k];
+    }
+}
+
+// the map through the TMA-in / streaming-store pipeline (qm_tma.cuh): the
+// input stream no longer waits on registers (the LDG kernel's stalls were on
+// the loads of v, not on the table); nodes 0..3599 of the centre in shared memory
+template <typename V> struct RodeVec;
+template <> struct RodeVec<double2> { using T = double; static constexpr int W = 2; };
+template <> struct RodeVec<float4> { using T = float; static constexpr int W = 4; };
+
+template <typename V>
+struct MapRode {
+    const double *tab;
+    const double *sm;
+    template <int PER>
+    QM_DEV void map_slice(V *a) const
+    {
+        using T = typename RodeVec<V>::T;
+        constexpr int W = RodeVec<V>::W;
+        T *e = reinterpret_cast<T *>(a);
+        double in[PER * W], out[PER * W];
+#pragma unroll
+        for (int k = 0; k < PER * W; ++k) in[k] = (double)e[k];
+        rode_map_batch<kRodeTlNodes, PER * W>(tab, sm, in, out);
+#pragma unroll
+        for (int k = 0; k < PER * W; ++k) e[k] = (T)out[k];
+    }
+};
+
+template <typename V>
+__global__ void __launch_bounds__(32 * (kRodeTlNC + 1), 1)
+k_rode_map_tl(const V *__restrict__ v, V *__restrict__ x, int64_t ntiles, const double *__restrict__ tab)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *sm = reinterpret_cast<double *>(smem_raw + kRodeTlTileBytes);
+    rode_stage_centre<kRodeTlNodes>(tab, sm);
+    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V>{tab, sm});
 }
 
 // base quantile Q0: u < p- -> log(u/p-)/(a+b); u > p- -> -log((1-u)/p+)/(a-b).
@@ -93,22 +222,39 @@ k_exp_base_quantile(const T *__restrict__ u, T *__restrict__ v, int64_t n, const
 
 // fused: Philox uniforms (qm_philox_uniform layout) -> Q0 -> Q
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512, 1)
 k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned long long c0,
               const double *__restrict__ tab)
 {
+    extern __shared__ __align__(16) double rode_sm[];
+    rode_stage_centre(tab, rode_sm);
     constexpr int W = (sizeof(T) == 4) ? 4 : 2;                 // samples per Philox block
     const int64_t nb = (n + W - 1) / W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
-        const uint4 w = philox_block(c0 + (unsigned long long)b, seed);
-        double u[4];
-        if (W == 4) { u[0] = u01_f32(w.x); u[1] = u01_f32(w.y); u[2] = u01_f32(w.z); u[3] = u01_f32(w.w); }
-        else { u[0] = u01_f64(w.x, w.y); u[1] = u01_f64(w.z, w.w); }
+    // two Philox blocks per iteration, every sample computed before the stores
+    // (the table gathers of all samples in flight together)
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b0 < nb; b0 += 2 * stride) {
+        double u[2 * W], r[2 * W];
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const int64_t i = b * W + k;
-            if (i < n) x[i] = (T)rode_eval(tab, exp_base_quantile(tab, u[k]));
+        for (int h = 0; h < 2; ++h) {
+            const uint4 w = philox_block(c0 + (unsigned long long)(b0 + h * stride), seed);
+            if (W == 4) {
+                u[4 * h] = u01_f32(w.x); u[4 * h + 1] = u01_f32(w.y); u[4 * h + 2] = u01_f32(w.z); u[4 * h + 3] = u01_f32(w.w);
+            } else {
+                u[2 * h] = u01_f64(w.x, w.y); u[2 * h + 1] = u01_f64(w.z, w.w);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 2 * W; ++k) u[k] = exp_base_quantile(tab, u[k]);
+        rode_map_batch<kRodeSmemNodes, 2 * W>(tab, rode_sm, u, r);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t b = b0 + h * stride;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int64_t i = b * W + k;
+                if (b < nb && i < n) x[i] = (T)r[W * h + k];
+            }
         }
     }
 }

@@ -47,6 +47,30 @@ def test_recycle_exp_to_target_vs_exact_map(kind, par):
     assert ulp_errors(g32, ex32, np.float32).max() <= 2.0
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pipeline_equals_ldg_kernel_and_oracle(dtype):
+    """2^23 + 37 base samples (+ specials inside the tiles): whole tiles run the TMA
+    pipeline with 3600 staged centre nodes per side, the remainder and a
+    misaligned view the LDG kernel (4097 staged nodes): both bitwise equal, and
+    sampled parity with the exact map."""
+    kind, par = O.HYPERBOLIC, [1.0, 0.5, 1.0]
+    tab = Q.qm_exp_target_table(kind, par)
+    v = _base_samples(kind, par, (1 << 23) + 37, seed=9)
+    v[:6] = [0.0, -0.0, np.inf, -np.inf, np.nan, 1.76 / 0.5]            # specials, the staged-node edge
+    v = v.astype(dtype)
+    vd = torch.from_numpy(np.concatenate([[dtype(0.5)], v]).astype(dtype)).cuda()
+    tiled = Q.qm_recycle_exp_to_hyperbolic(vd[1:].clone(), tab)
+    ldg = Q.qm_recycle_exp_to_hyperbolic(vd[1:], tab)                      # misaligned: LDG kernel
+    assert torch.equal(tiled.nan_to_num(), ldg.nan_to_num()) and torch.equal(tiled.isnan(), ldg.isnan())
+    idx = np.random.default_rng(4).choice(v.size - 6, 4096, replace=False) + 6
+    g = tiled.cpu().numpy()[idx].astype(np.float64)
+    ex = O.recycle_exp_to_target(kind, par, v[idx].astype(np.float64)).astype(np.float64)
+    if dtype == np.float64:
+        assert np.max(np.abs(g / ex - 1)) < 1e-14
+    else:
+        assert ulp_errors(g.astype(np.float32), ex, np.float32).max() <= 2.0
+
+
 def test_specials_and_fused_sampler():
     kind, par = O.HYPERBOLIC, [1.0, 0.5, 1.0]
     tab = Q.qm_exp_target_table(kind, par)

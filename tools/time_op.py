@@ -41,6 +41,15 @@ elif name == "mc":
     ks = list(np.linspace(50, 150, 17))
     rows = torch.empty((Q.qm_mc_row_count(n), 34), dtype=torch.float64, device="cuda")
     fn = lambda: Q.qm_mc_european_call(n, SEED, 0, 100.0, 0.05, 0.2, 1.0, ks, out=rows)
+elif name.startswith("rode_hyp"):
+    import numpy as np
+    from synth import inputs as I
+    n = 1 << 28
+    tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+    dt = np.float64 if name.endswith("f64") else np.float32
+    v = torch.from_numpy(I.laplace(n, dtype=dt)).cuda()
+    x = torch.empty_like(v)
+    fn = lambda: Q.qm_recycle_exp_to_hyperbolic(v, tab, out=x)
 else:
     raise SystemExit("unknown " + name)
 for _ in range(3):
