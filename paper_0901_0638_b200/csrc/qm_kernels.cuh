@@ -82,13 +82,7 @@ struct TmaCfg {
     static constexpr int UNROLL = UNROLL_;
     static_assert(TILE_ % (4 * 32 * NC_ * UNROLL_) == 0, "tile must split evenly over the consumer threads");
 };
-using TmaCfgA = TmaCfg<16, 4, 8192, 1>;      // 1 CTA/SM, 16 consumer warps, 128 KB
 using TmaCfgB = TmaCfg<16, 3, 8192, 2>;      // 2 CTAs/SM, 32 consumer warps, 2 x 96 KB
-using TmaCfgC = TmaCfg<31, 4, 7936, 1>;      // 1 CTA/SM, 31 consumer warps, 124 KB
-using TmaCfgD = TmaCfg<16, 3, 8192, 2, 2>;   // B with two float4 in flight per thread
-using TmaCfgE = TmaCfg<12, 4, 6144, 2>;      // 2 CTAs/SM, 24 consumer warps, 2 x 96 KB
-using TmaCfgH = TmaCfg<12, 2, 6144, 3>;      // 3 CTAs/SM, 36 consumer warps, 3 x 48 KB
-using TmaCfgI = TmaCfg<8, 3, 4096, 4>;       // 4 CTAs/SM, 32 consumer warps, 4 x 48 KB
 
 // one float4 of u -> one float4 of z: a single vote per warp picks the fast path
 // (no special-value code) or the careful path for all 4 x 32 samples
@@ -170,8 +164,6 @@ struct TlCfg {
 using TlCfgJ = TlCfg<16, 4, 8192, 1>;       // 1 CTA/SM, 16 consumer warps, 4 x 32 KB
 using TlCfgK = TlCfg<16, 3, 8192, 2>;       // 2 CTAs/SM, 2 x 3 x 32 KB
 using TlCfgL = TlCfg<16, 4, 8192, 1, 2>;    // J, 2 float4 per vote
-using TlCfgM = TlCfg<24, 4, 12288, 1, 2>;   // 1 CTA/SM, 24 consumer warps, 4 x 48 KB, 2 float4 per vote
-using TlCfgN = TlCfg<12, 4, 6144, 2, 2>;    // 2 CTAs/SM, 2 x 12 consumer warps, 2 x 4 x 24 KB, 2 float4 per vote
 
 template <int ALG, class CFG>
 __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
@@ -213,67 +205,6 @@ struct OpNormalF32 {
         }
     }
 };
-
-// Software-pipelined variant: the fp32 log of float4 j+1 is computed in the
-// same iteration as the FP64 rational of float4 j, so the FP32/ALU work of one
-// sample overlaps the FP64 chain of the previous one inside each thread.
-template <int ALG, class CFG>
-struct OpNormalF32Pipe {
-    QM_DEV static void logs(const float4 a, float4 &zl, float4 &om)
-    {
-        om = make_float4(__fsub_rn(1.0f, a.x), __fsub_rn(1.0f, a.y), __fsub_rn(1.0f, a.z), __fsub_rn(1.0f, a.w));
-        const float2 l01 = neg_log2x_f32x2(fminf(a.x, om.x), fminf(a.y, om.y));
-        const float2 l23 = neg_log2x_f32x2(fminf(a.z, om.z), fminf(a.w, om.w));
-        zl = make_float4(l01.x, l01.y, l23.x, l23.y);
-    }
-    QM_DEV static bool normal(const float4 a)
-    {
-        constexpr float m = fast_vv_min_f32<ALG>();
-        return (fminf(a.x, __fsub_rn(1.0f, a.x)) >= m) & (fminf(a.y, __fsub_rn(1.0f, a.y)) >= m) &
-               (fminf(a.z, __fsub_rn(1.0f, a.z)) >= m) & (fminf(a.w, __fsub_rn(1.0f, a.w)) >= m);
-    }
-    QM_DEV void tile(float *t, int ctid, int nct) const
-    {
-        float4 *t4 = reinterpret_cast<float4 *>(t);
-        constexpr int per = CFG::TILE / 4 / (CFG::NC * 32);
-        // a whole tile is normal for every grid input; otherwise take the careful path
-        bool ok = true;
-#pragma unroll 4
-        for (int j = 0; j < per; ++j) ok &= normal(t4[ctid + j * nct]);
-        if (!__all_sync(0xffffffffu, ok)) {
-#pragma unroll 1
-            for (int j = 0; j < per; ++j) {
-                float4 *p = t4 + ctid + j * nct;
-                const float4 a = *p;
-                *p = make_float4(nq_f32_careful<ALG>(a.x), nq_f32_careful<ALG>(a.y), nq_f32_careful<ALG>(a.z),
-                                 nq_f32_careful<ALG>(a.w));
-            }
-            return;
-        }
-        float4 a = t4[ctid], zl, om;
-        logs(a, zl, om);
-#pragma unroll 1
-        for (int j = 0; j < per; ++j) {
-            float4 an = a, zn = zl, omn = om;
-            if (j + 1 < per) {
-                an = t4[ctid + (j + 1) * nct];
-                logs(an, zn, omn);
-            }
-            t4[ctid + j * nct] = make_float4(apply_sign_f32(rat32<ALG>(zl.x), a.x, om.x),
-                                             apply_sign_f32(rat32<ALG>(zl.y), a.y, om.y),
-                                             apply_sign_f32(rat32<ALG>(zl.z), a.z, om.z),
-                                             apply_sign_f32(rat32<ALG>(zl.w), a.w, om.w));
-            a = an; zl = zn; om = omn;
-        }
-    }
-};
-
-template <int ALG, class CFG>
-__global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)
-k_normal_f32_tma_pipe(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
-{
-    tma_stream_map<float, CFG::TILE, CFG::STAGES, CFG::NC>(u, z, ntiles, OpNormalF32Pipe<ALG, CFG>{});
-}
 
 template <int ALG, class CFG>
 __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)

@@ -109,24 +109,13 @@ qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64
     return launched();
 }
 
-// QM_TMA_CFG=A|B|C selects the pipeline shape (A/B diagnostics; default B)
-char tma_cfg()
-{
-    static char c = 0;
-    if (!c) {
-        const char *e = getenv("QM_TMA_CFG");
-        c = (e && e[0] >= 'A' && e[0] <= 'I') ? e[0] : 'B';
-    }
-    return c;
-}
-
-// QM_TL_CFG=J..N selects the TMA-in/STG-out shape (default L)
+// QM_TL_CFG=J|K|L selects the TMA-in/STG-out shape (default L)
 char tl_cfg()
 {
     static char c = 0;
     if (!c) {
         const char *e = getenv("QM_TL_CFG");
-        c = (e && e[0] >= 'J' && e[0] <= 'N') ? e[0] : 'L';
+        c = (e && e[0] >= 'J' && e[0] <= 'L') ? e[0] : 'L';
     }
     return c;
 }
@@ -140,22 +129,11 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
         switch (tl_cfg()) {
         case 'K': return launch_stream_f32<TlCfgK>(k_normal_f32_tl<ALG, TlCfgK>, k_normal_f32<ALG>, u, z, n, s);
         case 'L': return launch_stream_f32<TlCfgL>(k_normal_f32_tl<ALG, TlCfgL>, k_normal_f32<ALG>, u, z, n, s);
-        case 'M': return launch_stream_f32<TlCfgM>(k_normal_f32_tl<ALG, TlCfgM>, k_normal_f32<ALG>, u, z, n, s);
-        case 'N': return launch_stream_f32<TlCfgN>(k_normal_f32_tl<ALG, TlCfgN>, k_normal_f32<ALG>, u, z, n, s);
         default: return launch_stream_f32<TlCfgJ>(k_normal_f32_tl<ALG, TlCfgJ>, k_normal_f32<ALG>, u, z, n, s);
         }
     }
-    switch (tma_cfg()) {
-    case 'A': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
-    case 'C': return launch_stream_f32<TmaCfgC>(k_normal_f32_tma<ALG, TmaCfgC>, k_normal_f32<ALG>, u, z, n, s);
-    case 'D': return launch_stream_f32<TmaCfgD>(k_normal_f32_tma<ALG, TmaCfgD>, k_normal_f32<ALG>, u, z, n, s);
-    case 'E': return launch_stream_f32<TmaCfgE>(k_normal_f32_tma<ALG, TmaCfgE>, k_normal_f32<ALG>, u, z, n, s);
-    case 'F': return launch_stream_f32<TmaCfgB>(k_normal_f32_tma_pipe<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
-    case 'G': return launch_stream_f32<TmaCfgA>(k_normal_f32_tma_pipe<ALG, TmaCfgA>, k_normal_f32<ALG>, u, z, n, s);
-    case 'H': return launch_stream_f32<TmaCfgH>(k_normal_f32_tma<ALG, TmaCfgH>, k_normal_f32<ALG>, u, z, n, s);
-    case 'I': return launch_stream_f32<TmaCfgI>(k_normal_f32_tma<ALG, TmaCfgI>, k_normal_f32<ALG>, u, z, n, s);
-    default: return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
-    }
+    // QM_STREAM_PATH=tma: the first (in-place, bulk-store) pipeline, shape B
+    return launch_stream_f32<TmaCfgB>(k_normal_f32_tma<ALG, TmaCfgB>, k_normal_f32<ALG>, u, z, n, s);
 }
 
 template <int ALG>
@@ -163,7 +141,7 @@ qm_status exp2n_f32(const float *v, float *z, int64_t n, cudaStream_t s)
 {
     if (stream_path() == 2)
         return launch_stream_f32<TlCfgJ>(k_exp2n_f32_tl<ALG, TlCfgJ>, k_exp2n_f32<ALG>, v, z, n, s);
-    return launch_stream_f32<TmaCfgA>(k_exp2n_f32_tma<ALG, TmaCfgA>, k_exp2n_f32<ALG>, v, z, n, s);
+    return launch_stream_f32<TmaCfgB>(k_exp2n_f32_tma<ALG, TmaCfgB>, k_exp2n_f32<ALG>, v, z, n, s);
 }
 
 #define QM_ALG_LAST QM_TWO_REGION

@@ -1,5 +1,5 @@
 """Max ulp of the fp32 breakless map over the whole fp32 odd grid (2^24 values)
-for the current QM_TMA_CFG (experiment helper)."""
+for the current library build (QM_LIB_PATH) and stream path (experiment helper)."""
 import os
 import sys
 
@@ -17,4 +17,4 @@ lo = np.ldexp(2 * k + 1, -24).astype(np.float32)
 u = np.concatenate([lo, (1 - lo.astype(np.float64)).astype(np.float32)])
 g = Q.qm_normal_quantile(torch.from_numpy(u).cuda()).cpu().numpy()
 ref = O.normal_breakless(u.astype(np.float64), O.C55, 32)
-print(os.environ.get("QM_TMA_CFG"), summary(ulp_errors(g, ref, np.float32)))
+print(os.environ.get("QM_LIB_PATH", "default"), summary(ulp_errors(g, ref, np.float32)))

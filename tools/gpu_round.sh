@@ -5,7 +5,7 @@ mkdir -p gpurun_out/profiles
 nvidia-smi -L > gpurun_out/gpu.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+t0=$(date +%s); timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench wall $(( $(date +%s) - t0 )) s" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 prof() {  # name regex [env] [prof_kernel name]
   timeout 600 env $3 ncu --set full --clock-control none --import-source on -k regex:$2 -s 1 -c 1 \
@@ -22,7 +22,7 @@ for k in ${PROFS:-}; do
     fused_f64) prof fused_f64 k_philox_f64 ;;
     student) prof student k_student_f64_tl ;;
     exp2n_f32) prof exp2n_f32 k_exp2n_f32_tl ;;
-    rode_hyp_f64) prof rode_hyp_f64 k_rode_map ;;
+    rode_hyp_f64) prof rode_hyp_f64 k_rode_map_tl ;;
     rode_philox_f32) prof rode_philox_f32 k_rode_philox ;;
     two_region) prof two_region k_normal_f32_tl "" stream_f32_two ;;
   esac
