@@ -348,13 +348,21 @@ def dist_variants(torch, dist, rank, world, steps=5, warmup=2):
     out = {}
     strikes = list(np.linspace(50, 150, 17))
 
-    def run(name, fn, n_total):
+    def run(name, fn, n_total, collective="all_reduce(SUM) of the fixed-chunk row matrix (NCCL)"):
         ms = max_over_ranks(time_steps(fn, steps, warmup, dist), dist) / steps
         r = fn()
         out[name] = {"gsamples_s": n_total / (ms / 1e3) / 1e9, "ms": ms, "n": n_total, "n_gpus": world,
-                     "scaling": "strong", "collective": "all_reduce(SUM) of the fixed-chunk row matrix (NCCL)",
+                     "scaling": "strong", "collective": collective,
                      "result": [float(x) for x in (r[0] if isinstance(r, tuple) else r).flatten()[:4].cpu()]}
 
+    # config 3: Philox-fused 2^32 fp32 normals, fixed total split by counter ranges
+    # (no collective: every rank writes its own slice; bit-identical to one GPU)
+    nloc = (1 << 32) // world
+    zloc = torch.empty(nloc, dtype=torch.float32, device="cuda")
+    import paper_0901_0638_b200 as Q
+    run("dist_fused_f32_2^32", lambda: (Q.qm_normal_philox(nloc, SEED, rank * (nloc // 4), out=zloc)[:4],), 1 << 32,
+        collective="none (counter-range shards)")
+    del zloc
     run("dist_student_moments_f64_nu5_2^30",
         lambda: S.student_moments(1 << 30, 5.0, 16, 4.6506, SEED, rank, world)[0], 1 << 30)
     run("dist_mc_call_sweep_2^34_17K",
