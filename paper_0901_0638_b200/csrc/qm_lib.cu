@@ -526,14 +526,15 @@ qm_status qm_moments(const void *x, int64_t n, qm_precision p, int kmax, double 
 
 // ------------------------------------------------------------------ e2e
 namespace {
+constexpr int kHostPipeMax = 4;
 struct HostPipe {
-    cudaStream_t st[2] = {nullptr, nullptr};
-    void *din[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
+    cudaStream_t st[kHostPipeMax] = {};
+    void *din[kHostPipeMax] = {}, *dout[kHostPipeMax] = {};
     size_t cap = 0;   // bytes per buffer
-    int dev = -1;
+    int dev = -1, np = 0;
     ~HostPipe()
     {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kHostPipeMax; ++i) {
             if (din[i]) cudaFree(din[i]);
             if (dout[i]) cudaFree(dout[i]);
             if (st[i]) cudaStreamDestroy(st[i]);
@@ -550,26 +551,37 @@ qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, q
     if (!normal_supported(p, alg)) return QM_EUNSUPPORTED;
     if (n == 0) return QM_OK;
     const size_t es = (p == QM_F32) ? 4 : 8;
-    const int64_t chunk = (int64_t)1 << 24;                 // elements per pipeline stage
+    // QM_HOST_STREAMS (2..4) x chunks of 2^QM_HOST_CHUNK_LOG2 elements (A/B knobs)
+    static int np_cfg = -1, lg_cfg = -1;
+    if (np_cfg < 0) {
+        const char *e = getenv("QM_HOST_STREAMS"), *f = getenv("QM_HOST_CHUNK_LOG2");
+        np_cfg = e ? atoi(e) : 2;
+        lg_cfg = f ? atoi(f) : 24;
+        if (np_cfg < 2 || np_cfg > kHostPipeMax) np_cfg = 2;
+        if (lg_cfg < 20 || lg_cfg > 27) lg_cfg = 24;
+    }
+    const int NP = np_cfg;
+    const int64_t chunk = (int64_t)1 << lg_cfg;             // elements per pipeline stage
     const size_t need = (size_t)chunk * es;
     HostPipe &hp = g_pipe;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (hp.dev != dev || hp.cap < need) {
+    if (hp.dev != dev || hp.cap < need || hp.np != NP) {
         hp.~HostPipe();
         new (&hp) HostPipe();
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NP; ++i) {
             if (cudaStreamCreateWithFlags(&hp.st[i], cudaStreamNonBlocking) != cudaSuccess) return QM_ECUDA;
             if (cudaMalloc(&hp.din[i], need) != cudaSuccess || cudaMalloc(&hp.dout[i], need) != cudaSuccess)
                 return QM_ECUDA;
         }
         hp.cap = need;
         hp.dev = dev;
+        hp.np = NP;
     }
     const char *hu = (const char *)u_host;
     char *hz = (char *)z_host;
     int k = 0;
-    for (int64_t off = 0; off < n; off += chunk, k ^= 1) {
+    for (int64_t off = 0; off < n; off += chunk, k = (k + 1) % NP) {
         const int64_t m = (n - off < chunk) ? (n - off) : chunk;
         cudaStream_t s = hp.st[k];
         if (cudaMemcpyAsync(hp.din[k], hu + off * es, m * es, cudaMemcpyHostToDevice, s) != cudaSuccess) return QM_ECUDA;
@@ -577,7 +589,7 @@ qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, q
         if (r != QM_OK) return r;
         if (cudaMemcpyAsync(hz + off * es, hp.dout[k], m * es, cudaMemcpyDeviceToHost, s) != cudaSuccess) return QM_ECUDA;
     }
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < NP; ++i)
         if (cudaStreamSynchronize(hp.st[i]) != cudaSuccess) return QM_ECUDA;
     return QM_OK;
 }
