@@ -494,6 +494,7 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
         return launched();
     };
     if (nk <= 8) return go(k_mc_call<8>);
+    if (nk == 17) return go(k_mc_call<17, 1, 3, true>);
     if (nk <= 17) return go(k_mc_call<17, 1, 3>);
     return go(k_mc_call<32>);
 }

@@ -43,13 +43,16 @@ QM_DEV void flush_pair(double *acc, int tid, int q, int nk, float2 sum, float2 s
 // NKMAX: register budget for the per-thread fp32 partials (instantiated for 8, 17, 32)
 // MINB: resident blocks per SM the register budget is set for (17 strikes: 3
 // blocks at 80 registers, +3.5 % over 2 blocks at 96)
-template <int NKMAX, int VB = 1, int MINB = 1>
+// EXACT: the call has exactly NKMAX strikes, so the strike loop has no run-time
+// bounds (a warp-uniform branch per strike pair otherwise)
+template <int NKMAX, int VB = 1, int MINB = 1, bool EXACT = false>
 __global__ void __launch_bounds__(256, MINB)
 k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __grid_constant__ McParams mp,
           double *__restrict__ rows)
 {
     extern __shared__ double acc[];            // [2 * nk][256]
     const int nk = mp.nk, tid = threadIdx.x;
+    const int nkl = EXACT ? NKMAX : nk;        // the hot loop's strike count
     const PhiloxKeys keys(seed);
     for (int j = 0; j < 2 * nk; ++j) acc[j * 256 + tid] = 0.0;
 
@@ -93,12 +96,12 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
         for (int q = 0; q < NP; ++q) {
 #pragma unroll
             for (int k = 0; k < 4 * VB; ++k) {
-                if (2 * q + 1 < nk) {
+                if (2 * q + 1 < nkl) {
                     const float2 d = add2(make_float2(ST[k], ST[k]), make_float2(-mp.K[2 * q], -mp.K[2 * q + 1]));
                     const float2 p = make_float2(fmaxf(d.x, 0.0f), fmaxf(d.y, 0.0f));
                     sum[q] = add2(sum[q], p);
                     sq[q] = fma2(p, p, sq[q]);
-                } else if (2 * q < nk) {
+                } else if (2 * q < nkl) {
                     const float p = fmaxf(__fsub_rn(ST[k], mp.K[2 * q]), 0.0f);
                     sum[q].x = __fadd_rn(sum[q].x, p);
                     sq[q].x = __fmaf_rn(p, p, sq[q].x);
