@@ -122,6 +122,18 @@ def test_mc_rows_vs_oracle():
     assert np.all(np.abs(got - ref) <= 2e-5 * np.abs(ref) + 1e-3)
 
 
+@pytest.mark.parametrize("strikes", [[100.0], [80.0, 95.0, 100.0, 105.0, 120.0],
+                                     list(np.linspace(60, 140, 10)), list(np.linspace(40, 200, 32))])
+def test_mc_rows_other_strike_counts(strikes):
+    """The kernel instantiations for <= 8, <= 17 (run-time count) and <= 32 strikes
+    (the 17-strike bench case has its own exact instantiation, tested above)."""
+    n, seed, c0 = (1 << 18) + 77, 5, 3
+    rows = Q.qm_mc_european_call(n, seed, c0, 100.0, 0.05, 0.2, 1.0, strikes)
+    got = Q.qm_reduce_rows(rows).view(-1, 2).cpu().numpy()
+    ref = O.mc_call(n, seed, c0, 100.0, 0.05, 0.2, 1.0, strikes).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 2e-5 * np.abs(ref) + 1e-3)
+
+
 def test_mc_price_vs_black_scholes_and_device_count():
     """2^26 samples: every strike within 4 standard errors of Black-Scholes; the
     sweep gives the same bits when sharded over G = 1, 2, 4 ranks (emulated)."""
