@@ -301,6 +301,15 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
         rec(f"config1_f64_2^20_{name}", graph.replay, 100 << 20, 16,
             extra={"timing": "CUDA graph of 100 launches per step"})
     del u64, z64
+    # the paper's Table 3 speed-ups of the breakless App D kernel (context)
+    g = lambda k: out[f"config1_f64_2^20_{k}"]["gsamples_s"]
+    out["config1_speedups"] = {
+        "breakless_vs_as241": g("breakless_D13") / g("as241"),
+        "breakless_vs_acklam_refined": g("breakless_D13") / g("acklam_refined"),
+        "breakless_vs_acklam_l1": g("breakless_D13") / g("acklam"),
+        "paper_table3_vs_as241": {"Quadro FX 4800": 1.44, "GTX 285": 1.45, "GTX 480": 1.41},
+        "paper_table3_vs_acklam_lea": {"Quadro FX 4800": 2.69, "GTX 285": 2.71, "GTX 480": 2.61},
+        "note": "context only: the paper's timings are for an unstated N on sm_1.x/2.0 hardware (P:647)"}
     out["size_sweep"] = size_sweep(Q, torch)
     return out
 
