@@ -69,16 +69,23 @@ qm_status launched()
 
 bool bad_ptrs(const void *a, const void *b, int64_t n) { return n > 0 && (a == nullptr || b == nullptr); }
 
-// QM_STREAM_PATH (A/B diagnostics): "ldg" forces the register-pipelined LDG
-// kernels, "tma" the in-place TMA load/store pipeline; default "tl" (TMA in,
-// streaming stores out)
+// A/B diagnostic knobs, read once per process (function-local statics: their
+// initialisation is thread-safe)
+int env_int(const char *name, int dflt, int lo, int hi)
+{
+    const char *e = getenv(name);
+    const int v = e ? atoi(e) : dflt;
+    return (v < lo || v > hi) ? dflt : v;
+}
+
+// QM_STREAM_PATH: "ldg" forces the register-pipelined LDG kernels, "tma" the
+// in-place TMA load/store pipeline; default "tl" (TMA in, streaming stores out)
 int stream_path()
 {
-    static int p = -1;
-    if (p < 0) {
+    static const int p = [] {
         const char *e = getenv("QM_STREAM_PATH");
-        p = (e && strcmp(e, "ldg") == 0) ? 0 : (e && strcmp(e, "tma") == 0) ? 1 : 2;
-    }
+        return (e && strcmp(e, "ldg") == 0) ? 0 : (e && strcmp(e, "tma") == 0) ? 1 : 2;
+    }();
     return p;
 }
 bool tma_enabled() { return stream_path() != 0; }
@@ -112,11 +119,10 @@ qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64
 // QM_TL_CFG=J|K|L selects the TMA-in/STG-out shape (default L)
 char tl_cfg()
 {
-    static char c = 0;
-    if (!c) {
+    static const char c = [] {
         const char *e = getenv("QM_TL_CFG");
-        c = (e && e[0] >= 'J' && e[0] <= 'L') ? e[0] : 'L';
-    }
+        return (e && e[0] >= 'J' && e[0] <= 'L') ? e[0] : 'L';
+    }();
     return c;
 }
 
@@ -222,8 +228,7 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     // the pipeline only pays with several tiles per CTA (small n: the LDG kernel
     // balances better, e.g. config 1's 2^20: 55 vs 40 Gsamples/s)
     if (alg == QM_BREAKLESS && vec && stream_path() == 2 && n >= ((int64_t)1 << 23)) {
-        static int cfg = -1;   // QM_TL64_CFG (A/B): 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B
-        if (cfg < 0) { const char *e = getenv("QM_TL64_CFG"); cfg = e ? atoi(e) : 1; }
+        static const int cfg = env_int("QM_TL64_CFG", 1, 0, 2);   // 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B
         if (cfg > 0) {
             auto go = [&](auto k, int tile, int threads, size_t smem) {
                 const int64_t ntiles = n / tile;
@@ -553,14 +558,8 @@ qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n, q
     if (n == 0) return QM_OK;
     const size_t es = (p == QM_F32) ? 4 : 8;
     // QM_HOST_STREAMS (2..4) x chunks of 2^QM_HOST_CHUNK_LOG2 elements (A/B knobs)
-    static int np_cfg = -1, lg_cfg = -1;
-    if (np_cfg < 0) {
-        const char *e = getenv("QM_HOST_STREAMS"), *f = getenv("QM_HOST_CHUNK_LOG2");
-        np_cfg = e ? atoi(e) : 2;
-        lg_cfg = f ? atoi(f) : 24;
-        if (np_cfg < 2 || np_cfg > kHostPipeMax) np_cfg = 2;
-        if (lg_cfg < 20 || lg_cfg > 27) lg_cfg = 24;
-    }
+    static const int np_cfg = env_int("QM_HOST_STREAMS", 2, 2, kHostPipeMax);
+    static const int lg_cfg = env_int("QM_HOST_CHUNK_LOG2", 24, 20, 27);
     const int NP = np_cfg;
     const int64_t chunk = (int64_t)1 << lg_cfg;             // elements per pipeline stage
     const size_t need = (size_t)chunk * es;
