@@ -1,6 +1,10 @@
 // qm_kernels.cuh -- __global__ kernels of the hot path (sm_100a).
 //
-// All streaming kernels share one shape:
+// Large aligned arrays (>= 2^23 samples) stream through the TMA-in /
+// streaming-store pipeline of qm_tma.cuh (`*_tl` kernels: persistent CTAs,
+// bulk-copy input ring, per-warp stage release, one warp vote per group of
+// samples); everything else, and the remainder of the pipelines, runs the
+// register-pipelined LDG kernels below.  The LDG kernels share one shape:
 //  * grid = k x (SM count) blocks of 256 threads, a warp-uniform grid-stride
 //    loop over warp CHUNKS (32 lanes x V 128-bit vectors), so every branch in
 //    the loop body is warp-uniform -- the paper's divergence argument

@@ -17,6 +17,10 @@
 //
 // The producer runs up to S tiles ahead, so S * TILE bytes per SM are in
 // flight no matter how many registers the math uses.
+//
+// Two pipelines live here: tma_stream_map (the in-place design above, kept for
+// A/B runs, QM_STREAM_PATH=tma) and tma_load_map (below; the default): input by
+// TMA, stage released per warp right after its LDS, output by streaming stores.
 #pragma once
 #include "qm_math.cuh"
 
