@@ -1,0 +1,27 @@
+"""Small runs of every TMA-pipeline kernel for compute-sanitizer (memcheck / synccheck / racecheck)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_0901_0638_b200 as Q  # noqa: E402
+from synth import inputs as I  # noqa: E402
+
+n = (1 << 23) + 37
+u = torch.from_numpy(I.mixed_uniforms(n, dtype=np.float32)).cuda()
+Q.qm_normal_quantile(u)
+Q.qm_normal_quantile(u, alg=Q.TWO_REGION)
+Q.qm_recycle_exp_to_normal(torch.from_numpy(I.laplace(n, dtype=np.float32)).cuda())
+u64 = torch.from_numpy(I.mixed_uniforms(n, dtype=np.float64)).cuda()
+Q.qm_normal_quantile(u64)
+zn = torch.from_numpy(I.normals(n, dtype=np.float64)).cuda()
+Q.qm_recycle_normal_to_t(zn, 5.0, 16, 4.6506)
+tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+v = torch.from_numpy(I.laplace(n, dtype=np.float64)).cuda()
+Q.qm_recycle_exp_to_hyperbolic(v, tab)
+Q.qm_exp_target_philox(1 << 20, tab, 1, 0)
+Q.qm_mc_european_call(1 << 22, 1, 0, 100.0, 0.05, 0.2, 1.0, list(np.linspace(50, 150, 17)))
+torch.cuda.synchronize()
+print("sanitize run ok")
