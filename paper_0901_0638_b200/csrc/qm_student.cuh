@@ -72,10 +72,13 @@ QM_DEV double student_tail(const StudentParams &sp, double a)
     const dd lx = dd_log(erfcx(xh));
     dd logw = dd_add(dd{-x2.hi, -x2.lo}, lx);
     logw = dd_add(logw, dd{sp.logC_hi, sp.logC_lo});
-    // w^(-1/nu), w^(2/nu)
+    // w^(-1/nu) in double-double; w^(2/nu) enters only the correction
+    // 1 - (nu+1)/(2(nu+2)) w^(2/nu) (a term << 1 beside the leading 1), so double
+    // precision suffices for it: exp of the rounded exponent, relative error
+    // ~1e-15 of a term that is itself < 0.1 -> < 1e-16 of t
     const dd e1 = dd_exp(dd_mul(logw, dd{-sp.inv_nu, -sp.inv_nu_lo}));
-    const dd e2 = dd_exp(dd_mul(logw, dd{sp.two_over_nu, sp.two_over_nu_lo}));
-    const dd corr = dd_add_d(dd_mul_d(e2, -sp.acoef), 1.0);
+    const double e2 = exp(__dmul_rn(logw.hi + logw.lo, sp.two_over_nu));
+    const dd corr = two_sum(1.0, -__dmul_rn(e2, sp.acoef));
     const dd t = dd_mul(dd_mul(e1, dd{sp.sqrt_nu, sp.sqrt_nu_lo}), corr);
     return t.hi + t.lo;
 }

@@ -31,7 +31,8 @@ elif name == "fused_f64":
     fn = lambda: Q.qm_normal_philox(n, SEED, 0, dtype=torch.float64, out=z)
 elif name.startswith("student"):
     n = 1 << 30
-    nu, K, zs = {"student4": (4.0, 10, 3.93473), "student5": (5.0, 16, 4.6506)}[name]
+    nu, K, zs = {"student4": (4.0, 10, 3.93473), "student5": (5.0, 16, 4.6506), "student3": (3.0, 16, 3.5667),
+                 "student10": (10.0, 16, 6.9584)}[name]
     zn = Q.qm_normal_philox(n, SEED, 0, dtype=torch.float64)
     t = torch.empty_like(zn)
     fn = lambda: Q.qm_recycle_normal_to_t(zn, nu, K, zs, out=t)
