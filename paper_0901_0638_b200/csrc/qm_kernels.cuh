@@ -346,26 +346,37 @@ k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned
     }
 }
 
-template <int MODE, int ALG>
+template <int MODE, int ALG, int V = 1>   // V Philox blocks (2V samples) per lane per chunk
 __global__ void __launch_bounds__(kThreads)
 k_philox_f64(double *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
 {
+    const PhiloxKeys keys(seed);
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nb = (n + 1) >> 1;
-    const int64_t nchunks = (nb + 31) / 32;
+    const int64_t nchunks = (nb + 32 * V - 1) / (32 * V);
     for (int64_t c = gwarp; c < nchunks; c += nwarps) {
-        const int64_t b = c * 32 + lane;
-        const uint4 w = philox_block(c0 + (unsigned long long)b, seed);
-        double r0 = u01_f64(w.x, w.y), r1 = u01_f64(w.z, w.w);
-        if (MODE == 1) { r0 = nq_f64_fast<ALG>(r0); r1 = nq_f64_fast<ALG>(r1); }
-        const int64_t i = 2 * b;
-        if (vec && i + 1 < n) {
-            st_stream_d2(reinterpret_cast<double2 *>(z + i), make_double2(r0, r1));
-        } else {
-            if (i < n) z[i] = r0;
-            if (i + 1 < n) z[i + 1] = r1;
+        double r[2 * V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint4 w = philox_block(c0 + (unsigned long long)(c * 32 * V + 32 * j + lane), keys);
+            r[2 * j] = u01_f64(w.x, w.y);
+            r[2 * j + 1] = u01_f64(w.z, w.w);
+        }
+        if (MODE == 1) {
+#pragma unroll
+            for (int k = 0; k < 2 * V; ++k) r[k] = nq_f64_fast<ALG>(r[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const int64_t i = 2 * (c * 32 * V + 32 * j + lane);
+            if (vec && i + 1 < n) {
+                st_stream_d2(reinterpret_cast<double2 *>(z + i), make_double2(r[2 * j], r[2 * j + 1]));
+            } else {
+                if (i < n) z[i] = r[2 * j];
+                if (i + 1 < n) z[i + 1] = r[2 * j + 1];
+            }
         }
     }
 }
