@@ -385,8 +385,14 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # QM_DIST_BACKEND=gloo: a validation mode for boxes with fewer GPUs than
+        # ranks (ranks share devices; timings meaningless); the product is NCCL
+        backend = os.environ.get("QM_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     import paper_0901_0638_b200 as Q
