@@ -123,17 +123,23 @@ QM_DEV void normal_group_f32(float4 *a)
     float x[NS];
 #pragma unroll
     for (int j = 0; j < G; ++j) { x[4 * j] = a[j].x; x[4 * j + 1] = a[j].y; x[4 * j + 2] = a[j].z; x[4 * j + 3] = a[j].w; }
-    bool ok = true;
+    float om[NS], vv[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) ok &= (fminf(x[k], __fsub_rn(1.0f, x[k])) >= fast_vv_min_f32<ALG>());
+    for (int k = 0; k < NS; ++k) { om[k] = __fsub_rn(1.0f, x[k]); vv[k] = fminf(x[k], om[k]); }
+    // the whole group is "normal" iff the NaN-propagating minimum of its vv is
+    // >= the fast-path threshold: 3-input FMNMX3.NAN, one FSETP per group
+    float mn = vv[0];
+    int k0 = 1;
+#pragma unroll
+    for (; k0 + 1 < NS; k0 += 2) mn = min3_nan(mn, vv[k0], vv[k0 + 1]);
+    if (k0 < NS) mn = min_nan(mn, vv[k0]);
+    const bool ok = mn >= fast_vv_min_f32<ALG>();
     float y[NS];
     if (__all_sync(0xffffffffu, ok)) {
-        float om[NS], zl[NS];
+        float zl[NS];
 #pragma unroll
         for (int k = 0; k < NS; k += 2) {
-            om[k] = __fsub_rn(1.0f, x[k]);
-            om[k + 1] = __fsub_rn(1.0f, x[k + 1]);
-            const float2 lz = neg_log2x_f32x2(fminf(x[k], om[k]), fminf(x[k + 1], om[k + 1]));
+            const float2 lz = neg_log2x_f32x2(vv[k], vv[k + 1]);
             zl[k] = lz.x; zl[k + 1] = lz.y;
         }
 #pragma unroll

@@ -47,6 +47,20 @@ QM_DEV void st_stream_d2(double2 *p, double2 v)
 QM_DEV void st_stream(float4 *p, float4 v) { st_stream_f4(p, v); }
 QM_DEV void st_stream(double2 *p, double2 v) { st_stream_d2(p, v); }
 
+// NaN-propagating minima (min.NaN: FMNMX.NAN / 3-input FMNMX3.NAN on sm_100a)
+QM_DEV float min_nan(float a, float b)
+{
+    float d;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+QM_DEV float min3_nan(float a, float b, float c)
+{
+    float d;
+    asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 // Packed fp32 pair arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): two
 // independent IEEE round-to-nearest operations per instruction.
 QM_DEV float2 fma2(float2 a, float2 b, float2 c)
