@@ -123,9 +123,15 @@ QM_DEV void normal_group_f32(float4 *a)
     float x[NS];
 #pragma unroll
     for (int j = 0; j < G; ++j) { x[4 * j] = a[j].x; x[4 * j + 1] = a[j].y; x[4 * j + 2] = a[j].z; x[4 * j + 3] = a[j].w; }
+    // 1 - u two samples per FADD2 (the same IEEE subtraction per lane)
     float om[NS], vv[NS];
 #pragma unroll
-    for (int k = 0; k < NS; ++k) { om[k] = __fsub_rn(1.0f, x[k]); vv[k] = fminf(x[k], om[k]); }
+    for (int k = 0; k < NS; k += 2) {
+        const float2 o = add2(make_float2(1.0f, 1.0f), make_float2(-x[k], -x[k + 1]));
+        om[k] = o.x; om[k + 1] = o.y;
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) vv[k] = fminf(x[k], om[k]);
     // the whole group is "normal" iff the NaN-propagating minimum of its vv is
     // >= the fast-path threshold: 3-input FMNMX3.NAN, one FSETP per group
     float mn = vv[0];
@@ -142,8 +148,18 @@ QM_DEV void normal_group_f32(float4 *a)
             const float2 lz = neg_log2x_f32x2(vv[k], vv[k + 1]);
             zl[k] = lz.x; zl[k + 1] = lz.y;
         }
+        // sign of u - (1-u), two samples per FADD2 (+0 at u = 1/2, as apply_sign_f32)
+        float dsg[NS];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) y[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(zl[k]), x[k], om[k]);
+        for (int k = 0; k < NS; k += 2) {
+            const float2 d = add2(make_float2(x[k], x[k + 1]), make_float2(-om[k], -om[k + 1]));
+            dsg[k] = d.x; dsg[k + 1] = d.y;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const float mag = rat32<fast_alg<ALG>()>(zl[k]);
+            y[k] = __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
+        }
     } else {
 #pragma unroll
         for (int k = 0; k < NS; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
