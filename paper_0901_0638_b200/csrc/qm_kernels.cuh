@@ -344,16 +344,22 @@ k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned
             r[4 * j + 2] = u01_f32(w.z); r[4 * j + 3] = u01_f32(w.w);
         }
         if (MODE == 1) {
-            float om[4 * V], zl[4 * V];
+            // 1 - u and the sign subtraction two samples per FADD2 (same IEEE ops)
+            float om[4 * V], zl[4 * V], dsg[4 * V];
 #pragma unroll
             for (int k = 0; k < 4 * V; k += 2) {
-                om[k] = __fsub_rn(1.0f, r[k]);
-                om[k + 1] = __fsub_rn(1.0f, r[k + 1]);
+                const float2 o = add2(make_float2(1.0f, 1.0f), make_float2(-r[k], -r[k + 1]));
+                om[k] = o.x; om[k + 1] = o.y;
                 const float2 l = neg_log2x_f32x2(fminf(r[k], om[k]), fminf(r[k + 1], om[k + 1]));
                 zl[k] = l.x; zl[k + 1] = l.y;
+                const float2 d = add2(make_float2(r[k], r[k + 1]), make_float2(-om[k], -om[k + 1]));
+                dsg[k] = d.x; dsg[k + 1] = d.y;
             }
 #pragma unroll
-            for (int k = 0; k < 4 * V; ++k) r[k] = apply_sign_f32(rat32<fast_alg<ALG>()>(zl[k]), r[k], om[k]);
+            for (int k = 0; k < 4 * V; ++k) {
+                const float mag = rat32<fast_alg<ALG>()>(zl[k]);
+                r[k] = __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
+            }
         }
 #pragma unroll
         for (int j = 0; j < V; ++j) {
