@@ -1,4 +1,5 @@
 #!/bin/bash
+# (build the A/B libraries first: python -c "from paper_0901_0638_b200 import build as b; b.build(out='build/libqm_kc9.so', defines=['QM_D13_KC=9'])", likewise kc8)
 # fp64 D13: compensated-step count A/B (parity + speed)
 for lib in default build/libqm_kc9.so build/libqm_kc8.so; do
   if [ $lib = default ]; then env=""; else env="QM_LIB_PATH=$lib"; fi

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 rm -f gpurun_out/ab_*.json
 timeout 600 python -m pytest tests/test_gpu_normal.py tests/test_gpu_tail.py -q -rf > gpurun_out/pytest_ab.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_ab.txt
-for cfg in ${CFGS:-J K L M N}; do
+for cfg in ${CFGS:-J K L}; do
   QM_TL_CFG=$cfg timeout 300 python bench.py --no-variants --no-cpu-baseline > gpurun_out/ab_$cfg.json 2>gpurun_out/ab_$cfg.err
 done
 for lib in ${LIBS:-}; do
