@@ -287,18 +287,31 @@ k_normal_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n, in
 
 // fp64 map through the TMA-in / streaming-store pipeline: a lane's slice of PER
 // double2 under one vote per double2 (64 samples per warp vote)
-template <int ALG>
+#ifndef QM_F64_GROUP
+#define QM_F64_GROUP 1
+#endif
+template <int ALG, int GD = QM_F64_GROUP>   // GD double2 (2 GD samples) per lane per vote
 struct MapNormalF64 {
     template <int PER>
     QM_DEV void map_slice(double2 *a) const
     {
+        static_assert(PER % GD == 0, "group must divide the slice");
 #pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const double x0 = a[j].x, x1 = a[j].y;
-            const bool ok = (fmin(x0, __dadd_rn(1.0, -x0)) >= fast_vv_min_f64<ALG>()) &
-                            (fmin(x1, __dadd_rn(1.0, -x1)) >= fast_vv_min_f64<ALG>());
-            if (__all_sync(0xffffffffu, ok)) a[j] = make_double2(nq_f64_fast<ALG>(x0), nq_f64_fast<ALG>(x1));
-            else a[j] = make_double2(nq_f64_careful<ALG>(x0), nq_f64_careful<ALG>(x1));
+        for (int j = 0; j < PER; j += GD) {
+            bool ok = true;
+#pragma unroll
+            for (int g = 0; g < GD; ++g)
+                ok &= (fmin(a[j + g].x, __dadd_rn(1.0, -a[j + g].x)) >= fast_vv_min_f64<ALG>()) &
+                      (fmin(a[j + g].y, __dadd_rn(1.0, -a[j + g].y)) >= fast_vv_min_f64<ALG>());
+            if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+                for (int g = 0; g < GD; ++g)
+                    a[j + g] = make_double2(nq_f64_fast<ALG>(a[j + g].x), nq_f64_fast<ALG>(a[j + g].y));
+            } else {
+#pragma unroll
+                for (int g = 0; g < GD; ++g)
+                    a[j + g] = make_double2(nq_f64_careful<ALG>(a[j + g].x), nq_f64_careful<ALG>(a[j + g].y));
+            }
         }
     }
 };
