@@ -69,12 +69,44 @@ def test_ragged_and_misaligned(dtype, n, offset):
     assert (e.max() if e.size else 0.0) <= (4.0 if dtype == np.float32 else 2.0)
 
 
-def test_in_place():
-    u = I.mixed_uniforms(10000, dtype=np.float32)
+@pytest.mark.parametrize("alg", [Q.BREAKLESS, Q.BREAKLESS77, Q.BREAKLESS_TAIL])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_pipeline_equals_ldg_kernel(dtype, alg):
+    """qm.h promises results independent of the launch configuration: the TMA
+    pipelines (aligned, >= 2^23 samples; vote per 8 / 2 samples per lane) and the
+    LDG kernels (a misaligned view) give the same bits, specials included."""
+    u = I.mixed_uniforms((1 << 23) + 37, dtype=dtype)
+    x = torch.from_numpy(np.concatenate([[dtype(0.5)], u]).astype(dtype)).cuda()
+    tiled = Q.qm_normal_quantile(x[1:].clone(), alg=alg)
+    ldg = Q.qm_normal_quantile(x[1:], alg=alg)                     # 4/8-byte offset: misaligned
+    assert torch.equal(tiled.nan_to_num(), ldg.nan_to_num()) and torch.equal(tiled.isnan(), ldg.isnan())
+
+
+@pytest.mark.parametrize("n", [10000, (1 << 23) + 37])          # LDG kernels / TMA pipelines
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_in_place(n, dtype):
+    """out aliasing the input (qm.h: in-place allowed): every pipeline tile is read
+    by TMA before any consumer writes it, and tiles never overlap."""
+    u = I.mixed_uniforms(n, dtype=dtype)
     x = torch.from_numpy(u).cuda()
     ref = Q.qm_normal_quantile(x.clone()).cpu().numpy()
     Q.qm_normal_quantile(x, out=x)
     assert np.array_equal(x.cpu().numpy(), ref, equal_nan=True)
+    if dtype == np.float32:
+        v = torch.from_numpy(I.laplace(n, dtype=np.float32)).cuda()
+        ref = Q.qm_recycle_exp_to_normal(v.clone()).cpu().numpy()
+        Q.qm_recycle_exp_to_normal(v, out=v)
+        assert np.array_equal(v.cpu().numpy(), ref, equal_nan=True)
+    else:
+        zn = torch.from_numpy(I.normals(n, dtype=np.float64)).cuda()
+        ref = Q.qm_recycle_normal_to_t(zn.clone(), 5.0, 16, 4.6506).cpu().numpy()
+        Q.qm_recycle_normal_to_t(zn, 5.0, 16, 4.6506, out=zn)
+        assert np.array_equal(zn.cpu().numpy(), ref, equal_nan=True)
+        tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+        v = torch.from_numpy(I.laplace(n, dtype=np.float64)).cuda()
+        ref = Q.qm_recycle_exp_to_hyperbolic(v.clone(), tab).cpu().numpy()
+        Q.qm_recycle_exp_to_hyperbolic(v, tab, out=v)
+        assert np.array_equal(v.cpu().numpy(), ref, equal_nan=True)
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
