@@ -12,7 +12,7 @@ prof stream_f32 k_normal_f32_tl
 cp /tmp/prof_stream_f32.ncu-rep gpurun_out/ 2>/dev/null
 prof stream_f32_tma k_normal_f32_tma QM_STREAM_PATH=tma stream_f32
 prof stream_f32_ldg k_normal_f32 QM_STREAM_PATH=ldg stream_f32
-prof stream_f64 k_normal_f64
+prof stream_f64 k_normal_f64_tl
 prof fused_f32 k_philox_f32
 prof fused_f64 k_philox_f64
 prof student k_student_f64
