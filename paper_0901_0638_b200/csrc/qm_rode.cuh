@@ -60,27 +60,40 @@ struct RodePrep {
     double t, h, a, vmax;
 };
 
+// per-side segment boundaries Wc, V and Vmax, held in registers (loaded once
+// per thread): the segment choice needs no shared-memory load
+struct RodeBounds {
+    double wc0, wc1, v0, v1, vm0, vm1;
+};
+QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
+{
+    return RodeBounds{__ldg(tab + QM_RODE_SEG + 8), __ldg(tab + QM_RODE_SEG + 24 + 8),
+                      __ldg(tab + QM_RODE_SEG + 16), __ldg(tab + QM_RODE_SEG + 24 + 16),
+                      __ldg(tab + 28), __ldg(tab + 29)};
+}
+
 template <int M>
-QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double *sm)
+QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double *sm, const RodeBounds &bd)
 {
     const int side = (v < 0.0) ? 1 : 0;
     const double a = fabs(v);
-    const double *sg = sm + QM_RODE_SEG + 24 * side;            // 3 segment records of 8 doubles
-    const double vmax = sm[28 + side];
+    const double wc = side ? bd.wc1 : bd.wc0, vb = side ? bd.v1 : bd.v0;
     // segment j = [a >= Wc] + [a >= V] (selects; NaN lands in j = 0 and is replaced later)
-    const int j = (a >= sg[8]) + (a >= sg[16]);
-    const double *r = sg + 8 * j;                               // w0, h, 1/h, k0, n, w1
-    const double s = fmin((a - r[0]) * r[2], r[4]);             // local coordinate in [0, n]
-    const double fk = fmin(floor(s), r[4] - 1.0);
-    const int k = (int)r[3] + (int)fk;
+    const int j = (a >= wc) + (a >= vb);
+    // the segment record (w0, h | 1/h, k0 | n, w1) as three 16-byte shared loads
+    const double2 *r = reinterpret_cast<const double2 *>(sm + QM_RODE_SEG + 24 * side + 8 * j);
+    const double2 r01 = r[0], r23 = r[1], r45 = r[2];
+    const double s = fmin((a - r01.x) * r23.x, r45.x);          // local coordinate in [0, n]
+    const double fk = fmin(floor(s), r45.x - 1.0);
+    const int k = (int)r23.y + (int)fk;
     const bool in_sm = (M > 0) && (j == 0) && (k + 1 < M);
     RodePrep p;
     p.b = in_sm ? sm + kRodeSmHdr + 3 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
     p.st = in_sm ? 3 : 4;
     p.t = s - fk;
-    p.h = r[1];
+    p.h = r01.y;
     p.a = a;
-    p.vmax = vmax;
+    p.vmax = side ? bd.vm1 : bd.vm0;
     return p;
 }
 
@@ -122,7 +135,8 @@ QM_DEV double rode_special(double v, double q)
 // B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
 // issued before their arithmetic (4 keeps the state in registers)
 template <int M, int B>
-QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const double (&v)[B], double (&x)[B])
+QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const RodeBounds &bd, const double (&v)[B],
+                           double (&x)[B])
 {
     constexpr int G = B < 4 ? B : 4;
     static_assert(B % G == 0, "batch must split into groups of 4");
@@ -131,7 +145,7 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
         RodePrep p[G];
         RodeNodes nd[G];
 #pragma unroll
-        for (int k = 0; k < G; ++k) p[k] = rode_prep<M>(tab, v[g + k], sm);
+        for (int k = 0; k < G; ++k) p[k] = rode_prep<M>(tab, v[g + k], sm, bd);
 #pragma unroll
         for (int k = 0; k < G; ++k) nd[k] = rode_load<M>(p[k]);
 #pragma unroll
@@ -145,13 +159,14 @@ k_rode_map(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *
 {
     extern __shared__ __align__(16) double rode_sm[];
     rode_stage_centre(tab, rode_sm);
+    const RodeBounds bd = rode_bounds(tab);
     constexpr int U = 4;
     const int64_t S = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * S) {
         double a[U], r[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) a[k] = (i0 + k * S < n) ? (double)v[i0 + k * S] : 0.0;
-        rode_map_batch<kRodeSmemNodes, U>(tab, rode_sm, a, r);
+        rode_map_batch<kRodeSmemNodes, U>(tab, rode_sm, bd, a, r);
 #pragma unroll
         for (int k = 0; k < U; ++k)
             if (i0 + k * S < n) x[i0 + k * S] = (T)r[k];
@@ -169,6 +184,7 @@ template <typename V>
 struct MapRode {
     const double *tab;
     const double *sm;
+    RodeBounds bd;
     template <int PER>
     QM_DEV void map_slice(V *a) const
     {
@@ -178,7 +194,7 @@ struct MapRode {
         double in[PER * W], out[PER * W];
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) in[k] = (double)e[k];
-        rode_map_batch<kRodeTlNodes, PER * W>(tab, sm, in, out);
+        rode_map_batch<kRodeTlNodes, PER * W>(tab, sm, bd, in, out);
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) e[k] = (T)out[k];
     }
@@ -191,7 +207,7 @@ k_rode_map_tl(const V *__restrict__ v, V *__restrict__ x, int64_t ntiles, const 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sm = reinterpret_cast<double *>(smem_raw + kRodeTlTileBytes);
     rode_stage_centre<kRodeTlNodes>(tab, sm);
-    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V>{tab, sm});
+    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V>{tab, sm, rode_bounds(tab)});
 }
 
 // base quantile Q0: u < p- -> log(u/p-)/(a+b); u > p- -> -log((1-u)/p+)/(a-b).
@@ -228,6 +244,7 @@ k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned lo
 {
     extern __shared__ __align__(16) double rode_sm[];
     rode_stage_centre(tab, rode_sm);
+    const RodeBounds bd = rode_bounds(tab);
     constexpr int W = (sizeof(T) == 4) ? 4 : 2;                 // samples per Philox block
     const int64_t nb = (n + W - 1) / W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -246,7 +263,7 @@ k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned lo
         }
 #pragma unroll
         for (int k = 0; k < 2 * W; ++k) u[k] = exp_base_quantile(tab, u[k]);
-        rode_map_batch<kRodeSmemNodes, 2 * W>(tab, rode_sm, u, r);
+        rode_map_batch<kRodeSmemNodes, 2 * W>(tab, rode_sm, bd, u, r);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t b = b0 + h * stride;
