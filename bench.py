@@ -243,7 +243,12 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     z32 = torch.empty_like(u32)
     rec("stream_f32_F88_2^28", lambda: Q.qm_normal_quantile(u32, out=z32, alg=Q.BREAKLESS88), n, 8)
     rec("stream_f32_two_region_2^28", lambda: Q.qm_normal_quantile(u32, out=z32, alg=Q.TWO_REGION), n, 8)
-    del u32, z32
+    # row f2 (deep-tail composite; its fast path is App C) and row a4 (antithetic pairs:
+    # 4 B in, 8 B out per uniform; samples counted = outputs)
+    rec("stream_f32_tail_composite_2^28", lambda: Q.qm_normal_quantile(u32, out=z32, alg=Q.BREAKLESS_TAIL), n, 8)
+    za = torch.empty(2 * n, dtype=torch.float32, device="cuda")
+    rec("antithetic_f32_2^28_uniforms", lambda: Q.qm_normal_antithetic(u32, out=za), 2 * n, 6)
+    del u32, z32, za
     zf = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
     rec("philox_fused_f32_2^32", lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=zf), 1 << 32, 4, fact="fused_f32")
     del zf
