@@ -477,6 +477,46 @@ k_antithetic_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, 
     }
 }
 
+// antithetic pairs through the TMA pipeline: input float4 u -> two float4
+// (Z0, -Z0, Z1, -Z1), (Z2, -Z2, Z3, -Z3); the same arithmetic as k_antithetic_f32
+template <int ALG>
+struct MapAntithetic {
+    template <int PER>
+    QM_DEV void map_slice(const float4 *a, float4 *b) const
+    {
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const float x[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                ok &= (x[k] >= (ALG == ALG_BREAKLESS_TAIL ? 8.6e-17f : 1.17549435e-38f)) & (x[k] <= 1.0f);
+            float y[4];
+            if (__all_sync(0xffffffffu, ok)) {
+                const float2 l01 = neg_log2x_f32x2(x[0], x[1], -1);
+                const float2 l23 = neg_log2x_f32x2(x[2], x[3], -1);
+                y[0] = fabsf(rat32<fast_alg<ALG>()>(l01.x)); y[1] = fabsf(rat32<fast_alg<ALG>()>(l01.y));
+                y[2] = fabsf(rat32<fast_alg<ALG>()>(l23.x)); y[3] = fabsf(rat32<fast_alg<ALG>()>(l23.y));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) y[k] = anti_f32_careful<ALG>(x[k]);
+            }
+            b[2 * j] = make_float4(y[0], -y[0], y[1], -y[1]);
+            b[2 * j + 1] = make_float4(y[2], -y[2], y[3], -y[3]);
+        }
+    }
+};
+
+template <int ALG>
+__global__ void __launch_bounds__(32 * (16 + 1), 1)
+k_antithetic_f32_tl(const float *__restrict__ u, float *__restrict__ z, int64_t ntiles)
+{
+    tma_load_map<float4, 2048, 4, 16, MapAntithetic<ALG>, 2>(reinterpret_cast<const float4 *>(u),
+                                                            reinterpret_cast<float4 *>(z), ntiles,
+                                                            MapAntithetic<ALG>{});
+}
+
+
 template <int ALG>
 QM_DEV double anti_f64(double u)
 {

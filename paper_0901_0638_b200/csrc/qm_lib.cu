@@ -266,9 +266,27 @@ qm_status qm_normal_antithetic(const void *u, void *z, int64_t n, qm_precision p
     cudaStream_t s = (cudaStream_t)stream;
     if (p == QM_F32) {
         const int vec = aligned16(u) && aligned16(z);
-        const int g = grid_for(n, kThreads * 4, 8);
         return with_breakless(alg, [&](auto A) {
-            k_antithetic_f32<decltype(A)::value><<<g, kThreads, 0, s>>>((const float *)u, (float *)z, n, vec);
+            constexpr int ALG = decltype(A)::value;
+            const float *uf = (const float *)u;
+            float *zf = (float *)z;
+            int64_t done = 0;
+            if (vec && stream_path() == 2 && n >= ((int64_t)1 << 23)) {   // whole tiles: TMA pipeline
+                constexpr int64_t TILE = 8192;
+                const int64_t ntiles = n / TILE;
+                const size_t smem = (size_t)4 * TILE * sizeof(float);
+                auto k = k_antithetic_f32_tl<ALG>;
+                if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                    return QM_ECUDA;
+                const int sms = sm_count_for_current_device();
+                const int64_t gg = ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148);
+                k<<<(int)gg, 32 * 17, smem, s>>>(uf, zf, ntiles);
+                done = ntiles * TILE;
+            }
+            if (n > done) {
+                const int g = grid_for(n - done, kThreads * 4, 8);
+                k_antithetic_f32<ALG><<<g, kThreads, 0, s>>>(uf + done, zf + 2 * done, n - done, vec);
+            }
             return launched();
         });
     }

@@ -145,8 +145,9 @@ namespace qm {
 //   * no CTA-wide barrier per tile: a warp that finishes its slice goes on to
 //     the next tile without waiting for the other warps.
 //
-// OP::map_slice<PER>(V a[PER]) maps a lane's PER 16-byte vectors in place.
-template <typename V, int TILE_VECS, int STAGES, int NC, typename OP>
+// OP::map_slice<PER>(V a[PER]) maps a lane's PER 16-byte vectors in place; with
+// R > 1 outputs per input, OP::map_slice<PER>(a, b[R PER]) fills b instead.
+template <typename V, int TILE_VECS, int STAGES, int NC, typename OP, int R = 1>
 __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__restrict__ out, int64_t ntiles, OP op)
 {
     static_assert(sizeof(V) == 16, "16-byte vectors");
@@ -191,10 +192,21 @@ __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__rest
         for (int j = 0; j < PER; ++j) a[j] = tile[32 * j];
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        op.template map_slice<PER>(a);
-        V *o = out + t * TILE_VECS + off;
+        if constexpr (R == 1) {
+            op.template map_slice<PER>(a);
+            V *o = out + t * TILE_VECS + off;
 #pragma unroll
-        for (int j = 0; j < PER; ++j) st_stream(o + 32 * j, a[j]);
+            for (int j = 0; j < PER; ++j) st_stream(o + 32 * j, a[j]);
+        } else {
+            // R output vectors per input vector (input vector i -> outputs R i .. R i + R - 1)
+            V b[R * PER];
+            op.template map_slice<PER>(a, b);
+            V *o = out + (size_t)R * (t * TILE_VECS + off);
+#pragma unroll
+            for (int j = 0; j < PER; ++j)
+#pragma unroll
+                for (int r = 0; r < R; ++r) st_stream(o + R * 32 * j + r, b[R * j + r]);
+        }
         if (++s == STAGES) { s = 0; ph ^= 1; }
     }
 }

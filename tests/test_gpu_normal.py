@@ -139,9 +139,10 @@ def test_shards_concatenate_to_one_stream():
     assert torch.equal(torch.cat(parts), whole)
 
 
+@pytest.mark.parametrize("n", [50000, (1 << 23) + 37])          # LDG kernels / fp32 TMA pipeline
 @pytest.mark.parametrize("dtype,alg,formula,prec,bar", CASES)
-def test_antithetic(dtype, alg, formula, prec, bar):
-    u = np.concatenate([I.uniform_grid(50000, dtype=dtype), I.edge_values(dtype)])
+def test_antithetic(dtype, alg, formula, prec, bar, n):
+    u = np.concatenate([I.edge_values(dtype), I.uniform_grid(n, dtype=dtype), I.edge_values(dtype)])
     g = _gpu(Q.qm_normal_antithetic, u, alg=alg)
     ref = O.normal_antithetic(u.astype(np.float64), formula, prec)
     err = ulp_errors(g, ref, dtype)
@@ -237,3 +238,13 @@ def test_determinism_across_launches():
     a = Q.qm_normal_quantile(u)
     b = Q.qm_normal_quantile(u)
     assert torch.equal(a.nan_to_num(), b.nan_to_num())
+
+
+@pytest.mark.parametrize("alg", [Q.BREAKLESS, Q.BREAKLESS77, Q.BREAKLESS_TAIL])
+def test_antithetic_pipeline_equals_ldg(alg):
+    u = I.mixed_uniforms((1 << 23) + 37, dtype=np.float32)
+    x = torch.from_numpy(np.concatenate([[np.float32(0.5)], u])).cuda()
+    tiled = Q.qm_normal_antithetic(x[1:].clone(), alg=alg)
+    ldg = Q.qm_normal_antithetic(x[1:], alg=alg)                         # misaligned: LDG kernel
+    assert torch.equal(tiled.nan_to_num(), ldg.nan_to_num()) and torch.equal(tiled.isnan(), ldg.isnan())
+
