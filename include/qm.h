@@ -129,6 +129,17 @@ qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
 qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p,
                                  double nu, int K, double zstar, void *stream);
 
+/* Config 4 with fused moments: t as qm_recycle_normal_to_t (the
+ * same bits) and, in the same pass, the moment rows of qm_moment_rows below:
+ * rows[4 c + k - 1] = sum of t^k over the fixed chunk c of QM_MOMENT_CHUNK
+ * samples (k = 1..4), qm_moment_row_count(n) rows.  The rows are deterministic
+ * and independent of the device count (chunks align with the shards of the
+ * multi-GPU harness); their summation order inside a chunk differs from
+ * qm_moment_rows (equal to rounding).  fp64, K = 10 or 16 and 16-byte aligned
+ * arrays run one fused kernel; other cases run the map and qm_moment_rows. */
+qm_status qm_recycle_normal_to_t_moments(const void *z, void *t, int64_t n, qm_precision p, double nu, int K,
+                                         double zstar, double *rows, void *stream);
+
 /* Recycle two-sided (Laplace) exponential samples into normal samples
  * (P:397-405): z = sign(v) Q(|v|) with the breakless rational
  * and no logarithm.  +-0 -> +-0, +-inf -> +-inf, NaN -> NaN. */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "qm_philox_uniform": (_I32, [_P, _I64, _I32, _U64, _U64, _P]),
     "qm_normal_philox": (_I32, [_P, _I64, _I32, _I32, _U64, _U64, _P]),
     "qm_recycle_normal_to_t": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P]),
+    "qm_recycle_normal_to_t_moments": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P, _P]),
     "qm_recycle_exp_to_normal": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
     "qm_exp_target_table": (_I32, [_I32, _P, _P]),
     "qm_recycle_exp_to_hyperbolic": (_I32, [_P, _P, _I64, _I32, _P, _P]),

@@ -397,6 +397,45 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
     return launched();
 }
 
+qm_status qm_recycle_normal_to_t_moments(const void *z, void *t, int64_t n, qm_precision p, double nu, int K,
+                                         double zstar, double *rows, void *stream)
+{
+    if (n < 0 || bad_ptrs(z, t, n) || (n > 0 && rows == nullptr) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
+    if (!(nu > 0.0) || K < 1 || K > QM_STUDENT_KMAX) return QM_EINVAL;
+    if (!(zstar > 0.0)) {
+        if (nu == 4.0 && K == 10) zstar = 3.93473;
+        else return QM_EINVAL;
+    }
+    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
+    StudentParams sp;
+    if (!student_params(nu, K, zstar, &sp)) return QM_EUNSUPPORTED;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t done = 0;
+    if (p == QM_F64 && aligned16(z) && aligned16(t) && sp.kc == 3 && (K == 10 || K == 16)) {
+        // whole chunks: the map and the moment rows in one pass
+        const int64_t nchunks = n / QM_MOMENT_CHUNK;
+        if (nchunks > 0) {
+            const size_t smem = (size_t)kStudentStages * kStudentTileVecs * 16;
+            auto k = (K == 10) ? k_student_moments_tl<10, 3> : k_student_moments_tl<16, 3>;
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return QM_ECUDA;
+            const int sms = sm_count_for_current_device();
+            const int64_t g = nchunks < (sms > 0 ? sms : 148) ? nchunks : (sms > 0 ? sms : 148);
+            k<<<(int)g, 32 * (kStudentNC + 1), smem, s>>>((const double *)z, (double *)t, nchunks, sp, rows);
+            done = nchunks * QM_MOMENT_CHUNK;
+        }
+    }
+    if (n > done) {   // the rest: map, then the rows of the remaining chunks
+        const size_t es = (p == QM_F64) ? 8 : 4;
+        const qm_status r = qm_recycle_normal_to_t((const char *)z + done * es, (char *)t + done * es, n - done, p, nu,
+                                                   K, zstar, stream);
+        if (r != QM_OK) return r;
+        return moment_rows_launch((const char *)t + done * es, n - done, p == QM_F64, rows + 4 * (done / QM_MOMENT_CHUNK), s);
+    }
+    return launched();
+}
+
 qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev)
 {
     if (params == nullptr || table_dev == nullptr || (kind != QM_TARGET_HYPERBOLIC && kind != QM_TARGET_VG))

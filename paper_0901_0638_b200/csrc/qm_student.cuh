@@ -16,6 +16,7 @@
 #pragma once
 #include "qm_dd.cuh"
 #include "qm_tma.cuh"
+#include "qm_moments.cuh"
 
 #include "qm_student_params.h"
 
@@ -177,4 +178,103 @@ k_student_f64_tl(const double *__restrict__ z, double *__restrict__ t, int64_t n
         reinterpret_cast<const double2 *>(z), reinterpret_cast<double2 *>(t), ntiles, MapStudentF64<K, KC>{&sp});
 }
 
+// Config 4 with the moments fused into the map (SURVEY §8 d4 "Student-t ... with
+// fused moments S_1..S_4"): each CTA owns whole QM_MOMENT_CHUNK chunks (16 tiles
+// of 4096 samples, streamed by the TMA producer in order); a consumer warp maps
+// its slice of every tile, stores t, and accumulates x, x^2, x^3, x^4 of its
+// samples in a fixed order (tile, vector, component; the operations of
+// k_moment_rows).  At the chunk's end: a fixed xor-shuffle tree per warp, the
+// 16 warp partials added in warp order by warp 0, one row of 4 doubles per
+// chunk -- deterministic and independent of the grid, like qm_moment_rows (the
+// rows differ from its in summation order only).
+template <int K, int KC>
+__global__ void __launch_bounds__(32 * (kStudentNC + 1), 1)
+k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64_t nchunks,
+                     const __grid_constant__ StudentParams sp, double *__restrict__ rows)
+{
+    constexpr int TV = kStudentTileVecs, S = kStudentStages, NC = kStudentNC;
+    constexpr int TPC = QM_MOMENT_CHUNK / (2 * TV);                 // tiles per chunk
+    constexpr int PER = TV / (32 * NC);
+    constexpr uint32_t TILE_BYTES = TV * 16;
+    static_assert(TPC * 2 * TV == QM_MOMENT_CHUNK, "a chunk is a whole number of tiles");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *tiles = reinterpret_cast<double2 *>(smem_raw);
+    __shared__ __align__(8) uint64_t full[S], empty[S];
+    __shared__ double part[NC][4];
+    const double2 *z2 = reinterpret_cast<const double2 *>(z);
+    double2 *t2 = reinterpret_cast<double2 *>(t);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NC); }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            int64_t k = 0;
+            for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
+                for (int i = 0; i < TPC; ++i, ++k) {
+                    if (k >= S) mbar_wait(&empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+                    bulk_g2s(tiles + (size_t)st * TV, z2 + (c * TPC + i) * TV, TILE_BYTES, &full[st]);
+                    if (++st == S) { st = 0; ph ^= 1; }
+                }
+        }
+        return;
+    }
+    const int w = warp - 1;
+    const int off = w * (PER * 32) + lane;
+    const MapStudentF64<K, KC> op{&sp};
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+        for (int i = 0; i < TPC; ++i) {
+            mbar_wait(&full[st], ph);
+            const double2 *tile = tiles + (size_t)st * TV + off;
+            double2 a[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) a[j] = tile[32 * j];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            op.template map_slice<PER>(a);
+            double2 *o = t2 + (c * TPC + i) * TV + off;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                st_stream(o + 32 * j, a[j]);
+                const double v[2] = {a[j].x, a[j].y};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double v2 = __dmul_rn(v[e], v[e]);
+                    s1 = __dadd_rn(s1, v[e]);
+                    s2 = __dadd_rn(s2, v2);
+                    s3 = __fma_rn(v2, v[e], s3);
+                    s4 = __fma_rn(v2, v2, s4);
+                }
+            }
+            if (++st == S) { st = 0; ph ^= 1; }
+        }
+        // fixed xor tree: every lane ends with the same warp total
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            s1 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, d));
+            s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, d));
+            s3 = __dadd_rn(s3, __shfl_xor_sync(0xffffffffu, s3, d));
+            s4 = __dadd_rn(s4, __shfl_xor_sync(0xffffffffu, s4, d));
+        }
+        if (lane == 0) { part[w][0] = s1; part[w][1] = s2; part[w][2] = s3; part[w][3] = s4; }
+        consumer_bar(NC * 32);
+        if (w == 0 && lane < 4) {
+            double r = 0.0;
+            for (int q = 0; q < NC; ++q) r = __dadd_rn(r, part[q][lane]);
+            rows[c * 4 + lane] = r;
+        }
+        consumer_bar(NC * 32);                                      // part[] reused by the next chunk
+    }
+}
+
 }  // namespace qm
+

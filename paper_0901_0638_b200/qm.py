@@ -92,6 +92,23 @@ def qm_recycle_normal_to_t(z: torch.Tensor, nu: float, K: int = 16, zstar: float
     return t
 
 
+def qm_recycle_normal_to_t_moments(z: torch.Tensor, nu: float, K: int = 16, zstar: float = 0.0, out=None,
+                                   rows=None, stream=None):
+    """t = qm_recycle_normal_to_t(z) and its moment rows ((rows, 4) fp64) in one pass."""
+    _dev(z, "z")
+    t = _out(z, out)
+    nr = qm_moment_row_count(z.numel())
+    if rows is None:
+        rows = torch.empty((nr, 4), dtype=torch.float64, device=z.device)
+    _dev(rows, "rows")
+    if rows.dtype != torch.float64 or rows.numel() != 4 * nr:
+        raise ValueError("rows must be fp64 with 4 * qm_moment_row_count(n) elements")
+    L.check("qm_recycle_normal_to_t_moments", L.load().qm_recycle_normal_to_t_moments(
+        z.data_ptr(), t.data_ptr(), z.numel(), _prec(z), float(nu), int(K), float(zstar), rows.data_ptr(),
+        _stream(stream)))
+    return t, rows
+
+
 def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
     _dev(v, "v")
     z = _out(v, out)

@@ -73,10 +73,11 @@ def student_moments(n_total: int, nu: float, K: int, zstar: float, seed: int, ra
     itemsize = torch.tensor([], dtype=dtype).element_size()
     sh = shard(n_total, world, rank, itemsize)
     z = Q.qm_normal_philox(sh.count, seed, sh.counter_offset, dtype=dtype, device=device)
-    t = Q.qm_recycle_normal_to_t(z, nu, K, zstar)
-    rows = torch.zeros((global_rows(n_total), 4), dtype=torch.float64, device=t.device)
-    if sh.count:
-        Q.qm_moment_rows(t, out=rows[sh.row0:sh.row0 + sh.nrows])
+    rows = torch.zeros((global_rows(n_total), 4), dtype=torch.float64, device=z.device)
+    if sh.count:   # the map with the moment rows fused (one pass over t)
+        t, _ = Q.qm_recycle_normal_to_t_moments(z, nu, K, zstar, rows=rows[sh.row0:sh.row0 + sh.nrows])
+    else:
+        t = z
     allreduce_rows(rows, group)
     return Q.qm_reduce_rows(rows), t
 

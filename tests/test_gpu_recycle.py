@@ -90,6 +90,48 @@ def test_moment_rows_are_device_count_independent():
         assert torch.equal(rows, res[0][0]) and torch.equal(sums, res[0][1])
 
 
+@pytest.mark.parametrize("nu,K,zstar", [(4.0, 10, 3.93473), (3.0, 16, 3.5667), (10.0, 16, 6.9584)])
+def test_fused_moments_equal_map_and_rows(nu, K, zstar):
+    """qm_recycle_normal_to_t_moments: t bitwise equal to qm_recycle_normal_to_t;
+    rows equal to qm_moment_rows to rounding (whole chunks fused, a ragged last
+    chunk through the map + qm_moment_rows path, which is bitwise)."""
+    n = 37 * 65536 + 1234
+    zn = Q.qm_normal_philox(n, 77, 5, dtype=torch.float64)
+    zn[:11] = torch.tensor([0.0, -0.0, 1e-300, zstar, -zstar, 12.0, -20.0, 37.0, 5.0, -5.0, 8.0], dtype=torch.float64)
+    t, rows = Q.qm_recycle_normal_to_t_moments(zn, nu, K, zstar)
+    t_ref = Q.qm_recycle_normal_to_t(zn, nu, K, zstar)
+    assert torch.equal(t, t_ref)
+    rows_ref = torch.empty_like(rows)
+    Q.qm_moment_rows(t_ref, out=rows_ref)
+    absrows = torch.empty_like(rows)
+    Q.qm_moment_rows(t_ref.abs(), out=absrows)
+    # two summation orders of 65536 terms: |difference| <= 2 n eps sum |t|^k
+    # (t^4 of the deep-tail specials overflows to inf in both: compared exactly)
+    fin = torch.isfinite(rows_ref)
+    assert torch.equal(rows[~fin], rows_ref[~fin])
+    assert torch.all((rows - rows_ref).abs()[fin] <= 2 * 65536 * 2.2e-16 * absrows.abs()[fin] + 1e-300)
+    assert torch.equal(rows[-1], rows_ref[-1])                          # the ragged chunk: same kernel
+    again = Q.qm_recycle_normal_to_t_moments(zn, nu, K, zstar)[1]
+    assert torch.equal(again, rows)                                     # deterministic
+
+
+def test_fused_moment_rows_are_device_count_independent():
+    from paper_0901_0638_b200.shard import global_rows, shard
+    n = 5 * 65536 * 8 + 777
+    res = []
+    for G in (1, 2, 4, 8):
+        rows = torch.zeros((global_rows(n), 4), dtype=torch.float64, device="cuda")
+        for r in range(G):
+            sh = shard(n, G, r, 8)
+            if sh.count == 0:
+                continue
+            z = Q.qm_normal_philox(sh.count, 9, sh.counter_offset, dtype=torch.float64)
+            Q.qm_recycle_normal_to_t_moments(z, 5.0, 16, 4.6506, rows=rows[sh.row0:sh.row0 + sh.nrows])
+        res.append(rows.clone())
+    for rows in res[1:]:
+        assert torch.equal(rows, res[0])
+
+
 def test_student_moments_vs_oracle_and_theory():
     """Sums of t^k over the same Philox stream: GPU vs oracle (same formulas), and
     the sample moments vs E t^2 = nu/(nu-2), E t^4 = 3 nu^2/((nu-2)(nu-4)) (nu = 10)."""
