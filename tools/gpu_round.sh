@@ -25,6 +25,7 @@ for k in ${PROFS:-}; do
     rode_hyp_f64) prof rode_hyp_f64 k_rode_map_tl ;;
     rode_philox_f32) prof rode_philox_f32 k_rode_philox ;;
     two_region) prof two_region k_normal_f32_tl "" stream_f32_two ;;
+    student_moments) prof student_moments k_student_moments_tl ;;
   esac
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/launches.csv \

@@ -49,6 +49,11 @@ elif name == "mc":
     ks = list(np.linspace(50, 150, 17))
     rows = torch.empty((Q.qm_mc_row_count(1 << 32), 34), dtype=torch.float64, device="cuda")
     fn = lambda: Q.qm_mc_european_call(1 << 32, SEED, 0, 100.0, 0.05, 0.2, 1.0, ks, out=rows)
+elif name == "student_moments":
+    zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
+    t = torch.empty_like(zn)
+    rows = torch.empty((Q.qm_moment_row_count(1 << 30), 4), dtype=torch.float64, device="cuda")
+    fn = lambda: Q.qm_recycle_normal_to_t_moments(zn, 5.0, 16, 4.6506, out=t, rows=rows)
 elif name == "student":
     zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
     t = torch.empty_like(zn)
