@@ -238,6 +238,7 @@ k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64
             double2 a[PER];
 #pragma unroll
             for (int j = 0; j < PER; ++j) a[j] = tile[32 * j];
+            fence_proxy_async();                                    // generic reads before the next TMA write
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             op.template map_slice<PER>(a);

@@ -190,6 +190,9 @@ __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__rest
         V a[PER];
 #pragma unroll
         for (int j = 0; j < PER; ++j) a[j] = tile[32 * j];
+        // WAR across proxies: the generic-proxy reads of this stage must be
+        // ordered before the producer's next async-proxy (TMA) write into it
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if constexpr (R == 1) {
