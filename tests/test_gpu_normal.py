@@ -248,3 +248,21 @@ def test_antithetic_pipeline_equals_ldg(alg):
     ldg = Q.qm_normal_antithetic(x[1:], alg=alg)                         # misaligned: LDG kernel
     assert torch.equal(tiled.nan_to_num(), ldg.nan_to_num()) and torch.equal(tiled.isnan(), ldg.isnan())
 
+
+def test_ring_release_race_regression():
+    """Regression for the cross-proxy WAR race of the TMA ring: with
+    fresh buffers every run, a stage released before its generic reads were
+    fenced was sometimes refilled under a warp (one slice of the next tile's
+    inputs).  Twelve runs of the antithetic and plain pipelines must all equal the
+    LDG kernels bitwise."""
+    u = np.concatenate([I.edge_values(np.float32), I.uniform_grid((1 << 23) + 37, dtype=np.float32)])
+    x = torch.from_numpy(np.concatenate([[np.float32(0.5)], u])).cuda()
+    ref_a = Q.qm_normal_antithetic(x[1:])
+    ref_n = Q.qm_normal_quantile(x[1:])
+    import time
+    for _ in range(12):
+        time.sleep(0.1)                                   # an idle GPU between runs made it show
+        xa = torch.from_numpy(u).cuda()
+        assert torch.equal(Q.qm_normal_antithetic(xa).nan_to_num(), ref_a.nan_to_num())
+        assert torch.equal(Q.qm_normal_quantile(xa).nan_to_num(), ref_n.nan_to_num())
+
