@@ -10,7 +10,8 @@ import sys
 
 # elements per captured launch (tools/prof_kernel.py)
 ELEMS = {"stream_f32": 1 << 28, "stream_f32_ldg": 1 << 28, "stream_f64": 1 << 28, "fused_f32": 1 << 32,
-         "fused_f64": 1 << 31, "student": 1 << 30, "exp2n_f32": 1 << 28, "moments": 1 << 30, "mc": 1 << 32}
+         "fused_f64": 1 << 31, "student": 1 << 30, "exp2n_f32": 1 << 28, "moments": 1 << 30, "mc": 1 << 32,
+         "student_moments": 1 << 30, "two_region": 1 << 28, "rode_hyp_f64": 1 << 28, "rode_philox_f32": 1 << 28}
 
 d = sys.argv[1]
 out = {}
