@@ -38,10 +38,13 @@ WORKLOAD = ("configs[1]: 2^28 fp32 uniforms streamed from HBM -> branch-free nor
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
-                "source": "MEASURED_PEAKS.json (measured copy bandwidth, burst)"}
+        try:
+            with open(p) as f:
+                d = json.load(f)
+            return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                    "source": "MEASURED_PEAKS.json (measured copy bandwidth, burst)"}
+        except (OSError, ValueError, KeyError, TypeError):
+            pass
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)"}
 
 
