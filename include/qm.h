@@ -122,12 +122,26 @@ qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
  * and the two-term tail
  * t = sqrt(nu) w^(-1/nu)(1 - (nu+1)/(2(nu+2)) w^(2/nu)),
  * w = (1 - Phi(|z|)) nu sqrt(pi) Gamma(nu/2)/Gamma((nu+1)/2) for |z| >= zstar
- * (P:267-272), odd in z.  zstar <= 0 selects the paper's 3.93473 when nu = 4 and
- * K = 10 and is QM_EINVAL otherwise.  1 <= K <= 24; 1 <= nu <= 20
- * (the coefficient recurrence is ill-conditioned beyond, QM_EUNSUPPORTED).
- * +-inf -> +-inf, NaN -> NaN. */
+ * (P:267-272), odd in z.
+ * Validated configurations (zstar <= 0 selects the crossover from this table):
+ *     nu = 4,  K = 10, zstar = 3.93473 (the paper's; max rel. error 1.36e-5)
+ *     nu = 3,  K = 16, zstar = 3.5667  (4.2e-6)
+ *     nu = 5,  K = 16, zstar = 4.6506  (6.7e-6)
+ *     nu = 10, K = 16, zstar = 6.9584  (4.1e-6)
+ * (the last three: min-max crossovers of DESIGN.md reading R13, the paper gives
+ * only nu = 4).  zstar <= 0 with any other (nu, K) -> QM_EUNSUPPORTED.  A caller
+ * zstar > 0 is accepted for 1 <= nu <= 20, 1 <= K <= 24: the kernel then
+ * evaluates the same composite with the caller's crossover and its error is the
+ * caller's choice (tools/student_crossover.py computes min-max crossovers; the
+ * tests cover nu in {1.5, 2, 7, 20} x K in {10, 16, 24} that way).  nu outside
+ * [1, 20] -> QM_EUNSUPPORTED (the coefficient recurrence is ill-conditioned);
+ * nu <= 0, K outside [1, 24] or a NaN zstar -> QM_EINVAL.
+ * +-inf -> +-inf, NaN -> NaN; tail values beyond the double range -> +-inf. */
 qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p,
                                  double nu, int K, double zstar, void *stream);
+/* the crossover qm_recycle_normal_to_t uses for zstar <= 0, or 0 if (nu, K) is
+ * not a validated configuration (host-only, no CUDA call) */
+double qm_student_default_crossover(double nu, int K);
 
 /* Config 4 with fused moments: t as qm_recycle_normal_to_t (the
  * same bits) and, in the same pass, the moment rows of qm_moment_rows below:
@@ -225,10 +239,12 @@ qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double 
 int qm_rode_table_host(int kind, const double *params, double *table);
 
 /* End-to-end variant of qm_normal_quantile on HOST buffers: copies u in,
- * computes, copies z out, overlapping the three in chunks on library-owned
- * streams and pinned/device staging buffers (allocated once per thread and
- * reused).  Returns after z_host is complete.  Host buffers may be pageable or
- * pinned. */
+ * computes, copies z out in chunks on library-owned streams and device staging
+ * buffers (allocated once per thread and reused).  Returns after z_host is
+ * complete.  Host buffers may be pageable or pinned, but the copies overlap the
+ * kernels only when they are PINNED (cudaHostAlloc / torch pin_memory): with
+ * pageable memory each cudaMemcpyAsync is synchronous and the chunks run one
+ * after another. */
 qm_status qm_normal_quantile_host(const void *u_host, void *z_host, int64_t n,
                                   qm_precision p, qm_algorithm alg);
 

@@ -57,6 +57,7 @@ SIGNATURES = {
     "qm_moments": (_I32, [_P, _I64, _I32, _I32, _P, _P, _P]),
     "qm_normal_quantile_host": (_I32, [_P, _P, _I64, _I32, _I32]),
     "qm_student_coefficients": (_I32, [_D, _I32, _P]),
+    "qm_student_default_crossover": (_D, [_D, _I32]),
 }
 
 _lib = None

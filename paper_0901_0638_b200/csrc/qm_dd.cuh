@@ -72,11 +72,15 @@ QM_DEV dd dd_sqrt(dd a)
     return dd_norm(s, c);
 }
 
-// exp of a double-double, |x| < 700: k = round(x/ln2), r = x - k ln2 (dd),
+// exp of a double-double: k = round(x/ln2), r = x - k ln2 (dd),
 // exp(r) = 1 + r + r^2/2 + ... (Taylor to r^17, |r| <= 0.347) in dd for the
-// first terms; one final 2^k scaling.
+// first terms; one final 2^k scaling.  The argument is first clamped to
+// [-746, 710]: beyond, exp overflows to +inf / underflows to +0 through the
+// scaling (|k| <= 1077 keeps both exponent halves in range).
 QM_DEV dd dd_exp(dd x)
 {
+    if (x.hi > 710.0) x = dd{710.0, 0.0};           // +inf after scaling
+    if (x.hi < -746.0) x = dd{-746.0, 0.0};         // +0 after scaling
     const double k = rint(__dmul_rn(x.hi, 1.4426950408889634));
     // ln2 as a triple for an exact-enough reduction
     const double L1 = 6.93147180369123816490e-01, L2 = 1.90821492927058770002e-10, L3 = 1.1612227229362531851e-26;

@@ -139,7 +139,22 @@ QM_DEV void normal_group_f32(float4 *a)
 #pragma unroll
     for (; k0 + 1 < NS; k0 += 2) mn = min3_nan(mn, vv[k0], vv[k0 + 1]);
     if (k0 < NS) mn = min_nan(mn, vv[k0]);
-    const bool ok = mn >= fast_vv_min_f32<ALG>();
+    constexpr bool COMP = QM_F32_RAT >= 1 && fast_alg<ALG>() == ALG_BREAKLESS;
+    bool ok;
+    if constexpr (COMP) {
+        // the FMA-pipe rational needs every sample on the 24-bit lattice: 1 - (1 - u) == u
+        // (1 - u is exact for u >= 1/2, and for u < 1/2 exactly when u is a multiple of 2^-24)
+        float dm = 0.0f;
+#pragma unroll
+        for (int k = 0; k < NS; k += 2) {
+            const float2 b = add2(make_float2(1.0f, 1.0f), make_float2(-om[k], -om[k + 1]));
+            const float2 d = add2(b, make_float2(-x[k], -x[k + 1]));
+            dm = fmaxf(dm, fmaxf(fabsf(d.x), fabsf(d.y)));
+        }
+        ok = (mn >= QM_LATTICE_MIN) & (dm == 0.0f);
+    } else {
+        ok = mn >= fast_vv_min_f32<ALG>();
+    }
     float y[NS];
     if (__all_sync(0xffffffffu, ok)) {
         float zl[NS];
@@ -155,11 +170,20 @@ QM_DEV void normal_group_f32(float4 *a)
             const float2 d = add2(make_float2(x[k], x[k + 1]), make_float2(-om[k], -om[k + 1]));
             dsg[k] = d.x; dsg[k + 1] = d.y;
         }
+        float mag[NS];
 #pragma unroll
-        for (int k = 0; k < NS; ++k) {
-            const float mag = rat32<fast_alg<ALG>()>(zl[k]);
-            y[k] = __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
+        for (int k = 0; k < NS; k += 2) {
+            if (COMP && !(QM_F32_RAT == 2 && (k & 2) == 0)) {
+                const float2 m2 = c55_comp1_x2(make_float2(zl[k], zl[k + 1]));
+                mag[k] = m2.x; mag[k + 1] = m2.y;
+            } else {
+                mag[k] = rat32<fast_alg<ALG>()>(zl[k]);
+                mag[k + 1] = rat32<fast_alg<ALG>()>(zl[k + 1]);
+            }
         }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            y[k] = __uint_as_float((__float_as_uint(mag[k]) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
     } else {
 #pragma unroll
         for (int k = 0; k < NS; ++k) y[k] = nq_f32_careful<ALG>(x[k]);
@@ -368,11 +392,21 @@ k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned
                 const float2 d = add2(make_float2(r[k], r[k + 1]), make_float2(-om[k], -om[k + 1]));
                 dsg[k] = d.x; dsg[k + 1] = d.y;
             }
+            constexpr bool COMP = QM_F32_RAT >= 1 && fast_alg<ALG>() == ALG_BREAKLESS;
+            float mag[4 * V];
 #pragma unroll
-            for (int k = 0; k < 4 * V; ++k) {
-                const float mag = rat32<fast_alg<ALG>()>(zl[k]);
-                r[k] = __uint_as_float((__float_as_uint(mag) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
+            for (int k = 0; k < 4 * V; k += 2) {
+                if (COMP && !(QM_F32_RAT == 2 && (k & 2) == 0)) {   // grid inputs: always on the lattice
+                    const float2 m2 = c55_comp1_x2(make_float2(zl[k], zl[k + 1]));
+                    mag[k] = m2.x; mag[k + 1] = m2.y;
+                } else {
+                    mag[k] = rat32<fast_alg<ALG>()>(zl[k]);
+                    mag[k + 1] = rat32<fast_alg<ALG>()>(zl[k + 1]);
+                }
             }
+#pragma unroll
+            for (int k = 0; k < 4 * V; ++k)
+                r[k] = __uint_as_float((__float_as_uint(mag[k]) & 0x7fffffffu) | (__float_as_uint(dsg[k]) & 0x80000000u));
         }
 #pragma unroll
         for (int j = 0; j < V; ++j) {

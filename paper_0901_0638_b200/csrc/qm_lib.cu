@@ -173,11 +173,39 @@ qm_status with_breakless(qm_algorithm a, F f)
     }
 }
 
+// The validated Student configurations (qm.h): the paper's nu = 4, K = 10 with its
+// crossover 3.93473, and nu = 3, 5, 10 with K = 16 and the min-max
+// crossovers of reading R13 (tests/golden/student_crossover.txt).  zstar <= 0
+// selects from this table; a caller-supplied zstar > 0 is accepted for any
+// 1 <= nu <= 20, 1 <= K <= QM_STUDENT_KMAX (the caller owns the crossover).
+struct StudentDefault { double nu; int K; double zstar; };
+constexpr StudentDefault kStudentTable[] = {{4.0, 10, 3.93473}, {3.0, 16, 3.5667}, {5.0, 16, 4.6506}, {10.0, 16, 6.9584}};
+
+qm_status student_setup(double nu, int K, double zstar, StudentParams *sp)
+{
+    if (!(nu > 0.0) || K < 1 || K > QM_STUDENT_KMAX || zstar != zstar) return QM_EINVAL;
+    if (!(zstar > 0.0)) {
+        zstar = 0.0;
+        for (const StudentDefault &d : kStudentTable)
+            if (d.nu == nu && d.K == K) zstar = d.zstar;
+        if (zstar == 0.0) return QM_EUNSUPPORTED;   // no validated crossover for (nu, K)
+    }
+    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
+    return student_params(nu, K, zstar, sp) ? QM_OK : QM_EUNSUPPORTED;
+}
+
 }  // namespace
 
 extern "C" {
 
 int qm_abi_version(void) { return QM_ABI_VERSION; }
+
+double qm_student_default_crossover(double nu, int K)
+{
+    for (const StudentDefault &d : kStudentTable)
+        if (d.nu == nu && d.K == K) return d.zstar;
+    return 0.0;
+}
 
 const char *qm_status_string(qm_status s)
 {
@@ -363,14 +391,9 @@ qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision
                                  double zstar, void *stream)
 {
     if (n < 0 || bad_ptrs(z, t, n) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
-    if (!(nu > 0.0) || K < 1 || K > QM_STUDENT_KMAX) return QM_EINVAL;
-    if (!(zstar > 0.0)) {
-        if (nu == 4.0 && K == 10) zstar = 3.93473;
-        else return QM_EINVAL;
-    }
-    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
     StudentParams sp;
-    if (!student_params(nu, K, zstar, &sp)) return QM_EUNSUPPORTED;
+    const qm_status st = student_setup(nu, K, zstar, &sp);
+    if (st != QM_OK) return st;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     int64_t done = 0;
@@ -401,14 +424,9 @@ qm_status qm_recycle_normal_to_t_moments(const void *z, void *t, int64_t n, qm_p
                                          double zstar, double *rows, void *stream)
 {
     if (n < 0 || bad_ptrs(z, t, n) || (n > 0 && rows == nullptr) || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
-    if (!(nu > 0.0) || K < 1 || K > QM_STUDENT_KMAX) return QM_EINVAL;
-    if (!(zstar > 0.0)) {
-        if (nu == 4.0 && K == 10) zstar = 3.93473;
-        else return QM_EINVAL;
-    }
-    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
     StudentParams sp;
-    if (!student_params(nu, K, zstar, &sp)) return QM_EUNSUPPORTED;
+    const qm_status st = student_setup(nu, K, zstar, &sp);
+    if (st != QM_OK) return st;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
     int64_t done = 0;

@@ -224,6 +224,68 @@ QM_DEV float rational_f32path(float z, const double *P, const double *Q)
 #endif
 }
 
+// ---------------------------------------------- fp32 App C on the FMA pipe
+// z P(z)/Q(z) of App C (float coefficients) entirely in fp32, two
+// samples per instruction (FFMA2): plain Horner for the first four steps of P
+// and Q, the LAST step of each compensated (TwoProd by FMA, Fast2Sum of the
+// operands ordered by max/min: both positive, exact error), the quotient from
+// MUFU.RCP plus one residual correction (e = P - t Q with P's and Q's low parts)
+// folded into the final product z t + z (e r).  Valid for inputs on the 24-bit
+// lattice (vv a multiple of 2^-24, vv >= 2^-24, i.e. z <= 15.95): exhaustive CPU
+// emulation over every such vv with the kernel's log, rcp seed +-1 ulp: 3.64 ulp
+// max (tools/emu_f32map.c; off the lattice it reaches 4.5 ulp, so other inputs
+// take the FP64 evaluation).
+#define QM_C55P0F 1.2533136835212087879f
+#define QM_C55P1F 1.9797154223229267471f
+#define QM_C55P2F 0.80002295072483916762f
+#define QM_C55P3F 0.087403248265958578062f
+#define QM_C55P4F 0.0020751409553756572917f
+#define QM_C55P5F 4.744820732427972462e-6f
+#define QM_C55Q1F 2.0795584360534589311f
+#define QM_C55Q2F 1.2499328117341603014f
+#define QM_C55Q3F 0.23668431621373705623f
+#define QM_C55Q4F 0.0120098270559197768f
+#define QM_C55Q5F 0.00010590620919921025259f
+#define QM_LATTICE_MIN 5.9604644775390625e-8f      // 2^-24: the smallest vv on the lattice
+
+QM_DEV float rcp_approx_f32(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+QM_DEV float2 c55_comp1_x2(float2 z)
+{
+    float2 p = fma2(QM_C2(QM_C55P5F), z, QM_C2(QM_C55P4F));
+    float2 q = fma2(QM_C2(QM_C55Q5F), z, QM_C2(QM_C55Q4F));
+    p = fma2(p, z, QM_C2(QM_C55P3F));
+    q = fma2(q, z, QM_C2(QM_C55Q3F));
+    p = fma2(p, z, QM_C2(QM_C55P2F));
+    q = fma2(q, z, QM_C2(QM_C55Q2F));
+    p = fma2(p, z, QM_C2(QM_C55P1F));
+    q = fma2(q, z, QM_C2(QM_C55Q1F));
+    // last step: s = p z + a0 with its exact error (TwoProd + ordered Fast2Sum)
+    const float2 pp = mul2(p, z), qq = mul2(q, z);
+    const float2 ppe = fma2(p, z, make_float2(-pp.x, -pp.y)), qqe = fma2(q, z, make_float2(-qq.x, -qq.y));
+    const float2 ps = add2(pp, QM_C2(QM_C55P0F)), qs = add2(qq, QM_C2(1.0f));
+    const float2 tp = add2(ps, make_float2(-fmaxf(pp.x, QM_C55P0F), -fmaxf(pp.y, QM_C55P0F)));
+    const float2 tq = add2(qs, make_float2(-fmaxf(qq.x, 1.0f), -fmaxf(qq.y, 1.0f)));
+    const float2 ep = add2(make_float2(fminf(pp.x, QM_C55P0F), fminf(pp.y, QM_C55P0F)), make_float2(-tp.x, -tp.y));
+    const float2 eq = add2(make_float2(fminf(qq.x, 1.0f), fminf(qq.y, 1.0f)), make_float2(-tq.x, -tq.y));
+    const float2 lp = add2(ppe, ep), lq = add2(qqe, eq);
+    // quotient: t = ps r, e = ps + lp - t (qs + lq), result z t + z e r
+    const float2 r = make_float2(rcp_approx_f32(qs.x), rcp_approx_f32(qs.y));
+    const float2 t = mul2(ps, r);
+    float2 e = fma2(make_float2(-qs.x, -qs.y), t, ps);
+    e = add2(e, lp);
+    e = fma2(make_float2(-t.x, -t.y), lq, e);
+    return fma2(z, mul2(e, r), mul2(t, z));
+}
+
+// the same arithmetic for one sample (bitwise equal to a lane of c55_comp1_x2)
+QM_DEV float c55_comp1(float z) { return c55_comp1_x2(make_float2(z, z)).x; }
+
 // copysign by the sign of (u - (1-u)): +0 at u = 1/2 (P:773, P:855 sgn = +1)
 QM_DEV float apply_sign_f32(float mag, float u, float omu)
 {
@@ -374,6 +436,9 @@ enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5, ALG_F1212
 #define QM_TWO_BREAK_F32 10.0f
 #define QM_VC_F32 37.0f
 #define QM_VC_F64 86.75
+#ifndef QM_F32_RAT
+#define QM_F32_RAT 0     // fp32 App C fast path: 0 FP64 rational, 1 FMA-pipe (c55_comp1), 2 both (pairs alternate)
+#endif
 #ifndef QM_D13_KC
 #define QM_D13_KC 10     // compensated Horner steps of App D's 13 (A/B builds may override)
 #endif

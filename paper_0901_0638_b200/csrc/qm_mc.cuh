@@ -84,10 +84,21 @@ k_mc_call(int64_t n, unsigned long long seed, unsigned long long c0, const __gri
             const float2 vv = neg_log2x_f32x2(u01_f32(ws[k]), u01_f32(ws[k + 1]), -1);   // -log u
             v[k] = vv.x; v[k + 1] = vv.y;
         }
+        float zr[4 * VB];
+#pragma unroll
+        for (int k = 0; k < 4 * VB; k += 2) {
+            if (QM_F32_RAT >= 1 && !(QM_F32_RAT == 2 && (k & 2) == 0)) {   // grid u: v on the lattice's range
+                const float2 m2 = c55_comp1_x2(make_float2(v[k], v[k + 1]));
+                zr[k] = m2.x; zr[k + 1] = m2.y;
+            } else {
+                zr[k] = rat32<ALG_BREAKLESS>(v[k]);
+                zr[k + 1] = rat32<ALG_BREAKLESS>(v[k + 1]);
+            }
+        }
 #pragma unroll
         for (int k = 0; k < 4 * VB; ++k) {
             const int64_t i = 4 * (blk0 + 256 * (k / 4)) + (k % 4);
-            float z = rat32<ALG_BREAKLESS>(v[k]);
+            float z = zr[k];
             z = ((ws[k] >> 8) & 1u) ? z : -z;
             // past the end of the chunk: S_T = -inf makes every payoff max(-inf, 0) = 0
             ST[k] = (i < s1) ? expf(__fmaf_rn(mp.b, z, mp.a)) : __int_as_float(0xff800000);

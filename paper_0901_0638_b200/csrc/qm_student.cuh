@@ -69,6 +69,7 @@ QM_DEV double student_central_k(const StudentParams &sp, double a)
 // factors -- branch-free (libdevice exp() measured 2x slower in this kernel)
 QM_DEV double exp_plain(double x)
 {
+    x = fmin(fmax(x, -746.0), 710.0);              // saturate: +0 / +inf through the scaling
     const double k = rint(__dmul_rn(x, 1.4426950408889634));
     double r = __fma_rn(-k, 6.93147180369123816490e-01, x);
     r = __fma_rn(-k, 1.90821492927058770002e-10, r);
@@ -100,7 +101,9 @@ QM_DEV double student_tail(const StudentParams &sp, double a)
     const double e2 = exp_plain(__dmul_rn(logw.hi + logw.lo, sp.two_over_nu));
     const dd corr = two_sum(1.0, -__dmul_rn(e2, sp.acoef));
     const dd t = dd_mul(dd_mul(e1, dd{sp.sqrt_nu, sp.sqrt_nu_lo}), corr);
-    return t.hi + t.lo;
+    // beyond the double range w^(-1/nu) = +inf and the dd products' low parts are
+    // inf - inf = NaN: the value is +inf
+    return (t.hi == __longlong_as_double(0x7ff0000000000000LL)) ? t.hi : t.hi + t.lo;
 }
 
 template <int K = 0, int KC = 0>   // K = 0: run-time sp.K / sp.kc

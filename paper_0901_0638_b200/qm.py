@@ -11,6 +11,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib as L
+from ._lib import QMError  # noqa: F401
 
 BREAKLESS, BREAKLESS77, AS241, ACKLAM, ACKLAM_REFINED, BREAKLESS_TAIL, MORO = (
     L.QM_BREAKLESS, L.QM_BREAKLESS77, L.QM_AS241, L.QM_ACKLAM, L.QM_ACKLAM_REFINED, L.QM_BREAKLESS_TAIL, L.QM_MORO)
@@ -39,14 +40,37 @@ def _stream(stream) -> int:
     return getattr(stream, "cuda_stream", stream)
 
 
+def _buf(t: torch.Tensor, name: str, dtype, numel: int | None = None, min_numel: int | None = None) -> torch.Tensor:
+    """The one validator of every caller-supplied device buffer (out, rows, table):
+    a contiguous CUDA tensor of `dtype` with exactly `numel` (or at least
+    `min_numel`) elements -- the kernels write or read that many."""
+    _dev(t, name)
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{name} must have at least {min_numel} elements, got {t.numel()}")
+    return t
+
+
 def _out(x: torch.Tensor, out, numel: int | None = None, dtype=None) -> torch.Tensor:
     n = x.numel() if numel is None else numel
     if out is None:
         return torch.empty(n, dtype=dtype or x.dtype, device=x.device)
-    _dev(out, "out")
-    if out.numel() != n or out.dtype != (dtype or x.dtype):
-        raise ValueError("out has the wrong size or dtype")
+    _buf(out, "out", dtype or x.dtype, numel=n)
+    if out.device != x.device:
+        raise ValueError("out must be on the input's device")
     return out
+
+
+def _gen_out(out, n: int, dtype, device) -> torch.Tensor:
+    """Output of a generator entry point (no input tensor): n elements of dtype."""
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    if out is None:
+        return torch.empty(n, dtype=dtype, device=device or "cuda")
+    return _buf(out, "out", out.dtype if dtype is None else dtype, numel=n)
 
 
 def qm_normal_quantile(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
@@ -67,8 +91,7 @@ def qm_normal_antithetic(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream
 
 def qm_philox_uniform(n: int, seed: int, counter_offset: int = 0, dtype=torch.float32,
                       out=None, device=None, stream=None) -> torch.Tensor:
-    u = out if out is not None else torch.empty(n, dtype=dtype, device=device or "cuda")
-    _dev(u, "out")
+    u = _gen_out(out, n, None if out is not None else dtype, device)
     L.check("qm_philox_uniform", L.load().qm_philox_uniform(
         u.data_ptr(), n, _prec(u), seed, counter_offset, _stream(stream)))
     return u
@@ -76,33 +99,40 @@ def qm_philox_uniform(n: int, seed: int, counter_offset: int = 0, dtype=torch.fl
 
 def qm_normal_philox(n: int, seed: int, counter_offset: int = 0, dtype=torch.float32, alg: int = BREAKLESS,
                      out=None, device=None, stream=None) -> torch.Tensor:
-    z = out if out is not None else torch.empty(n, dtype=dtype, device=device or "cuda")
-    _dev(z, "out")
+    z = _gen_out(out, n, None if out is not None else dtype, device)
     L.check("qm_normal_philox", L.load().qm_normal_philox(
         z.data_ptr(), n, _prec(z), alg, seed, counter_offset, _stream(stream)))
     return z
 
 
-def qm_recycle_normal_to_t(z: torch.Tensor, nu: float, K: int = 16, zstar: float = 0.0,
+def _student_K(nu: float, K):
+    """K = None: the order of the validated configuration (qm.h): 10 for the paper's
+    nu = 4, 16 otherwise."""
+    return (10 if float(nu) == 4.0 else 16) if K is None else int(K)
+
+
+def qm_recycle_normal_to_t(z: torch.Tensor, nu: float, K: int | None = None, zstar: float = 0.0,
                            out=None, stream=None) -> torch.Tensor:
+    """zstar <= 0: the library's validated crossover for (nu, K) (qm.h), else
+    QMError(QM_EUNSUPPORTED); zstar > 0: the caller's crossover."""
     _dev(z, "z")
+    K = _student_K(nu, K)
     t = _out(z, out)
     L.check("qm_recycle_normal_to_t", L.load().qm_recycle_normal_to_t(
         z.data_ptr(), t.data_ptr(), z.numel(), _prec(z), float(nu), int(K), float(zstar), _stream(stream)))
     return t
 
 
-def qm_recycle_normal_to_t_moments(z: torch.Tensor, nu: float, K: int = 16, zstar: float = 0.0, out=None,
+def qm_recycle_normal_to_t_moments(z: torch.Tensor, nu: float, K: int | None = None, zstar: float = 0.0, out=None,
                                    rows=None, stream=None):
     """t = qm_recycle_normal_to_t(z) and its moment rows ((rows, 4) fp64) in one pass."""
     _dev(z, "z")
+    K = _student_K(nu, K)
     t = _out(z, out)
     nr = qm_moment_row_count(z.numel())
     if rows is None:
         rows = torch.empty((nr, 4), dtype=torch.float64, device=z.device)
-    _dev(rows, "rows")
-    if rows.dtype != torch.float64 or rows.numel() != 4 * nr:
-        raise ValueError("rows must be fp64 with 4 * qm_moment_row_count(n) elements")
+    _buf(rows, "rows", torch.float64, numel=4 * nr)
     L.check("qm_recycle_normal_to_t_moments", L.load().qm_recycle_normal_to_t_moments(
         z.data_ptr(), t.data_ptr(), z.numel(), _prec(z), float(nu), int(K), float(zstar), rows.data_ptr(),
         _stream(stream)))
@@ -144,9 +174,13 @@ def qm_rode_table_host(kind: int, params):
     return tab
 
 
+def _table(table: torch.Tensor) -> torch.Tensor:
+    return _buf(table, "table", torch.float64, numel=L.QM_RODE_TABLE_DOUBLES)
+
+
 def _rode_call(name, v, table, out, stream):
     _dev(v, "v")
-    _dev(table, "table")
+    _table(table)
     x = _out(v, out)
     L.check(name, getattr(L.load(), name)(v.data_ptr(), x.data_ptr(), v.numel(), _prec(v), table.data_ptr(),
                                           _stream(stream)))
@@ -167,8 +201,8 @@ def qm_exp_base_quantile(u: torch.Tensor, table: torch.Tensor, out=None, stream=
 
 def qm_exp_target_philox(n: int, table: torch.Tensor, seed: int, counter_offset: int = 0, dtype=torch.float64,
                          out=None, stream=None) -> torch.Tensor:
-    _dev(table, "table")
-    x = out if out is not None else torch.empty(n, dtype=dtype, device=table.device)
+    _table(table)
+    x = _gen_out(out, n, None if out is not None else dtype, table.device)
     L.check("qm_exp_target_philox", L.load().qm_exp_target_philox(x.data_ptr(), n, _prec(x), table.data_ptr(), seed,
                                                                   counter_offset, _stream(stream)))
     return x
@@ -189,8 +223,7 @@ def qm_mc_european_call(n: int, seed: int, counter_offset: int, S0: float, r: fl
     nr = qm_mc_row_count(n)
     rows = out if out is not None else torch.empty((max(nr, 1), 2 * len(ks)), dtype=torch.float64,
                                                    device=device or "cuda")
-    if rows.numel() < nr * 2 * len(ks):
-        raise ValueError("rows too small")
+    _buf(rows, "out", torch.float64, min_numel=nr * 2 * len(ks))
     L.check("qm_mc_european_call", L.load().qm_mc_european_call(n, seed, counter_offset, ctypes.byref(p),
                                                                 rows.data_ptr(), _stream(stream)))
     return rows
@@ -205,8 +238,7 @@ def qm_moment_rows(x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
     _dev(x, "x")
     nr = qm_moment_row_count(x.numel())
     rows = out if out is not None else torch.empty((nr, 4), dtype=torch.float64, device=x.device)
-    if rows.numel() < 4 * nr or rows.dtype != torch.float64:
-        raise ValueError("rows too small or not float64")
+    _buf(rows, "out", torch.float64, min_numel=4 * nr)
     L.check("qm_moment_rows", L.load().qm_moment_rows(x.data_ptr(), x.numel(), _prec(x), rows.data_ptr(),
                                                       _stream(stream)))
     return rows
@@ -214,9 +246,12 @@ def qm_moment_rows(x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
 
 def qm_reduce_rows(rows: torch.Tensor, out=None, stream=None) -> torch.Tensor:
     """Fixed-order column sums of a (nrows, ncol) fp64 matrix."""
-    _dev(rows, "rows")
+    _buf(rows, "rows", torch.float64)
+    if rows.dim() != 2:
+        raise ValueError("rows must be a (nrows, ncol) matrix")
     nrows, ncol = rows.shape
     o = out if out is not None else torch.empty(ncol, dtype=torch.float64, device=rows.device)
+    _buf(o, "out", torch.float64, min_numel=ncol)
     L.check("qm_reduce_rows", L.load().qm_reduce_rows(rows.data_ptr(), nrows, ncol, o.data_ptr(), _stream(stream)))
     return o
 
@@ -226,7 +261,9 @@ def qm_moments(x: torch.Tensor, kmax: int = 4, out=None, rows=None, stream=None)
     _dev(x, "x")
     nr = qm_moment_row_count(x.numel())
     ws = rows if rows is not None else torch.empty(max(nr, 1) * 4, dtype=torch.float64, device=x.device)
+    _buf(ws, "rows", torch.float64, min_numel=4 * nr)
     o = out if out is not None else torch.empty(kmax, dtype=torch.float64, device=x.device)
+    _buf(o, "out", torch.float64, min_numel=kmax)
     L.check("qm_moments", L.load().qm_moments(x.data_ptr(), x.numel(), _prec(x), kmax, o.data_ptr(),
                                               ws.data_ptr(), _stream(stream)))
     return o
@@ -242,6 +279,11 @@ def qm_normal_quantile_host(u: torch.Tensor, out=None, alg: int = BREAKLESS) -> 
     L.check("qm_normal_quantile_host", L.load().qm_normal_quantile_host(
         u.data_ptr(), z.data_ptr(), u.numel(), _prec(u), alg))
     return z
+
+
+def qm_student_default_crossover(nu: float, K: int) -> float:
+    """The shipped crossover of a validated (nu, K) (qm.h), 0.0 if none."""
+    return L.load().qm_student_default_crossover(float(nu), int(K))
 
 
 def qm_student_coefficients(nu: float, K: int):

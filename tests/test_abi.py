@@ -57,7 +57,13 @@ def test_argument_validation_before_launch(lib):
     assert lib.qm_normal_quantile(p, p, 0, L.QM_F32, 0, None) == L.QM_OK       # n = 0: no-op
     assert lib.qm_normal_antithetic(p, p, 4, L.QM_F64, L.QM_ACKLAM, None) == L.QM_EUNSUPPORTED
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, -1.0, 10, 0.0, None) == L.QM_EINVAL
-    assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 5.0, 16, 0.0, None) == L.QM_EINVAL   # zstar needed
+    # zstar <= 0: the validated table (qm.h); (5, 10) is not in it
+    assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 5.0, 10, 0.0, None) == L.QM_EUNSUPPORTED
+    assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 7.0, 16, -1.0, None) == L.QM_EUNSUPPORTED
+    assert lib.qm_recycle_normal_to_t(p, p, 0, L.QM_F64, 5.0, 16, 0.0, None) == L.QM_OK
+    assert lib.qm_recycle_normal_to_t(p, p, 0, L.QM_F64, 7.0, 16, 5.6185, None) == L.QM_OK   # caller zstar
+    assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 5.0, 16, float("nan"), None) == L.QM_EINVAL
+    assert lib.qm_recycle_normal_to_t_moments(p, p, 4, L.QM_F64, 5.0, 10, 0.0, p, None) == L.QM_EUNSUPPORTED
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 50.0, 16, 5.0, None) == L.QM_EUNSUPPORTED
     assert lib.qm_recycle_normal_to_t(p, p, 4, L.QM_F64, 4.0, 0, 3.9, None) == L.QM_EINVAL
     assert lib.qm_moments(p, 10, L.QM_F64, 5, p, p, None) == L.QM_EINVAL
@@ -81,3 +87,34 @@ def test_student_host_coefficients_match_oracle(lib, nu, K):
     # last coefficient (weight c_16 z^32 / t < 1e-20 on |z| < z*) may be 2 ulp off
     tol = 1 if nu <= 10 else 2
     assert np.all(np.abs(got - ref_d) <= tol * np.spacing(np.abs(ref_d))), (got - ref_d) / np.spacing(np.abs(ref_d))
+
+
+def test_student_validated_table_matches_the_golden_crossovers(lib):
+    """The crossovers the library ships (zstar <= 0) are the paper's and the
+    oracle-computed min-max ones of tests/golden/student_crossover.txt (reading R13)."""
+    rows = [l.split() for l in (ROOT / "tests" / "golden" / "student_crossover.txt").read_text().splitlines()
+            if l.strip() and not l.startswith("#")]
+    shipped = [r for r in rows if len(r) == 4]
+    assert len(shipped) == 4
+    for nu, K, zs, _ in shipped:
+        assert lib.qm_student_default_crossover(float(nu), int(K)) == float(zs)
+    assert lib.qm_student_default_crossover(4.0, 10) == 3.93473
+    assert lib.qm_student_default_crossover(4.0, 16) == 0.0
+    assert lib.qm_student_default_crossover(7.0, 16) == 0.0
+
+
+def test_binding_validates_buffers_before_the_library():
+    """qm.py routes every out/rows/table through one validator: CPU tensors, wrong
+    dtypes and wrong sizes are rejected before any call into libqm (no fallback)."""
+    import torch
+    from paper_0901_0638_b200 import qm
+    t = torch.zeros(4)
+    with pytest.raises(ValueError, match="CUDA"):
+        qm.qm_normal_quantile(t)
+    with pytest.raises(ValueError, match="CUDA"):
+        qm.qm_normal_philox(4, 1, out=t)
+    with pytest.raises(ValueError, match="CUDA"):
+        qm.qm_mc_european_call(1 << 20, 1, 0, 100.0, 0.05, 0.2, 1.0, [100.0], out=torch.zeros(2, dtype=torch.float64))
+    with pytest.raises(ValueError, match="CUDA"):
+        qm._table(torch.zeros(8, dtype=torch.float64))
+    assert qm._student_K(4.0, None) == 10 and qm._student_K(5.0, None) == 16 and qm._student_K(5.0, 24) == 24

@@ -28,7 +28,13 @@ def minmax_crossover(n, K):
     return z[s], tot[s]
 
 
+# caller-supplied crossovers tested beside the shipped table (qm.h): nu x K grid
+CALLER_GRID = [(n, K) for n in (1.5, 2.0, 7.0, 20.0) for K in (10, 16, 24)]
+
 if __name__ == "__main__":
     for n, K in [(3.0, 16), (5.0, 16), (10.0, 16)]:
         zs, e = minmax_crossover(n, K)
         print(f"{int(n):<5d} {K:<4d} {zs:.4f}   {e:.3e}")
+    for n, K in CALLER_GRID:
+        zs, e = minmax_crossover(n, K)
+        print(f"caller {n:<5g} {K:<4d} {zs:.4f}   {e:.3e}")
