@@ -212,10 +212,15 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
  *    down to v = 0 -- forward integration is exponentially ill-conditioned --
  *    and the first unit of rate*|v| redone forward from the exact centre
  *    conditions), then a synchronous copy (~1 MB; tens of ms of host work
- *    per parameter set).  params: hyperbolic {alpha, beta, delta}
- *    (alpha > |beta|, delta > 0); VG {lambda, alpha, beta} with integer
- *    1 <= lambda <= 9 (half-integer Bessel orders; lambda = 1 is the identity,
- *    P:395).  Otherwise QM_EINVAL / QM_EUNSUPPORTED (non-integer lambda).
+ *    per parameter set; ~4 s for a non-integer VG lambda).  params: hyperbolic
+ *    {alpha, beta, delta} (alpha > |beta|, delta > 0); VG {lambda, alpha, beta},
+ *    alpha > |beta|, with lambda = 1 (the identity), integer 2..9
+ *    (half-integer Bessel orders in closed form) or real 1.1 <= lambda <= 30
+ *    (K of real order by Temme's series / Steed's continued fraction; the
+ *    origin, where the density is not analytic for non-integer lambda, is
+ *    approached on a geometric mesh -- the "many steps near v = 0" of P:395).
+ *    Bad parameters -> QM_EINVAL; lambda < 1 (out of scope),
+ *    1 < lambda < 1.1 or lambda > 30 -> QM_EUNSUPPORTED.
  *  - qm_recycle_exp_to_hyperbolic / qm_recycle_exp_to_vg: x[i] = Q(v[i]) for
  *    base samples v (quintic Hermite on (Q, Q', Q'') at 24577 nodes per side:
  *    4096 on the centre rate*|v| <= 2, 16384 out to base probability e^-40,

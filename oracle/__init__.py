@@ -92,6 +92,7 @@ def lib():
             "orc_target_density": (i32, [i32, P, P, P, i64]),
             "orc_recycle_exp_to_target": (i32, [i32, P, P, P, i64]),
             "orc_exp_to_normal_tail": (i32, [P, P, i64, i32, i32, dbl]),
+            "orc_besselk_ld": (None, [dbl, dbl, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -205,7 +206,8 @@ HYPERBOLIC, VG = 1, 2
 
 
 def target_masses(kind: int, params):
-    """(p-, p+, Z) of the hyperbolic (params alpha, beta, delta) or VG (lambda, alpha, beta) target."""
+    """(p-, p+, Z) of the hyperbolic (params alpha, beta, delta) or VG (lambda, alpha, beta) target
+    (VG: any real lambda >= 1; P:395 puts lambda < 1 out of scope)."""
     p = _in(params); o = np.zeros(3, np.longdouble)
     _chk(lib().orc_target_masses(kind, _p(p), _p(o)))
     return o
@@ -215,6 +217,14 @@ def target_density(kind: int, params, x) -> np.ndarray:
     p = _in(params); x = _in(x); o = np.empty(x.shape, np.longdouble)
     _chk(lib().orc_target_density(kind, _p(p), _p(x), _p(o), x.size))
     return o
+
+
+def besselk(nu: float, z: float):
+    """K_nu(z) (long double) by the trapezoidal rule on its integral representation
+    (A&S 9.6.24) -- the VG density's Bessel function for non-integer lambda."""
+    o = np.zeros(1, np.longdouble)
+    lib().orc_besselk_ld(nu, z, _p(o))
+    return o[0]
 
 
 def recycle_exp_to_target(kind: int, params, v) -> np.ndarray:

@@ -6,8 +6,14 @@
  * The oracle states the map by its DEFINITION: Q(v) = F^-1(F0(v)), with
  *   base f0(x) = p+ (a-b) e^{-(a-b)x} (x > 0), p- (a+b) e^{(a+b)x} (x < 0)
  *   hyperbolic f(x) ~ exp(-a sqrt(d^2 + x^2) + b x)
- *   VG (integer lambda = m+1 >= 1; reading R25): f(x) ~ e^{bx} |x|^{lambda-1/2} K_{lambda-1/2}(a|x|)
- *      = e^{bx - a|x|} sum_{k=0}^{m} (m+k)!/(k!(m-k)!) (2a)^{-k} |x|^{m-k}   (K half-integer, A&S 10.2.15)
+ *   VG: f(x) ~ e^{bx} |x|^{nu} K_{nu}(a|x|), nu = lambda - 1/2, lambda >= 1
+ *      integer lambda = m+1 <= 9: the half-integer closed form (A&S 10.2.15)
+ *      = e^{bx - a|x|} sum_{k=0}^{m} (m+k)!/(k!(m-k)!) (2a)^{-k} |x|^{m-k};
+ *      any other lambda (reading R29): K_nu by its integral representation
+ *      K_nu(z) = int_0^inf exp(-z cosh t) cosh(nu t) dt (A&S 9.6.24) with the
+ *      trapezoidal rule (the integrand is entire and decays double-exponentially,
+ *      so the rule converges geometrically in 1/h: error ~ exp(-2 pi^2/(h^2 z))
+ *      relative for large z, exp(-pi^2/h) otherwise; h = min(1/8, 1/(2 sqrt z))).
  * p+- = target masses of x > 0 / x < 0, computed here by
  * adaptive Gauss-Kronrod (7-15) quadrature of the unnormalised density; the
  * tail masses by the same quadrature; Q by bracketed bisection on the TAIL
@@ -20,11 +26,33 @@
 #include <float.h>
 #include "orc.h"
 
-typedef struct { int kind; ld a, b, d; int m; } tgt_t;   /* kind 1 hyperbolic, 2 VG */
+typedef struct { int kind; ld a, b, d; int m; ld nu; } tgt_t;   /* kind 1 hyperbolic, 2 VG; m < 0: real lambda */
+
+/* K_nu(z), z > 0, by the trapezoidal rule on int_0^inf exp(-z cosh t) cosh(nu t) dt */
+static ld besselk_trap(ld nu, ld z)
+{
+    const ld h = (z > 16.0L) ? 0.5L / sqrtl(z) : 0.125L;
+    ld s = 0.5L * expl(-z);                              /* t = 0 (half weight: the integrand is even) */
+    for (int k = 1; k < 1000000; ++k) {
+        const ld t = (ld)k * h;
+        const ld term = expl(-z * coshl(t)) * coshl(nu * t);
+        s += term;
+        if (z * sinhl(t) > nu && term <= 1e-22L * s) break;   /* past the peak, converged */
+    }
+    return h * s;
+}
+
+double orc_besselk(double nu, double z) { return (double)besselk_trap((ld)nu, (ld)z); }
+void orc_besselk_ld(double nu, double z, ld *out) { *out = besselk_trap((ld)nu, (ld)z); }
 
 static ld dens_u(const tgt_t *t, ld x)                   /* unnormalised density */
 {
     if (t->kind == 1) return expl(-t->a * sqrtl(t->d * t->d + x * x) + t->b * x);
+    if (t->m < 0) {                                      /* real lambda: e^{bx} |x|^nu K_nu(a|x|) */
+        const ld ax = fabsl(x);
+        if (ax == 0.0L) return tgammal(t->nu) * powl(2.0L, t->nu - 1.0L) * powl(t->a, -t->nu);   /* the limit */
+        return expl(t->b * x) * powl(ax, t->nu) * besselk_trap(t->nu, t->a * ax);
+    }
     ld ax = fabsl(x), s = 0.0L, fact_mk = 1.0L;
     /* sum_{k=0}^{m} (m+k)!/(k!(m-k)!) (2a)^-k |x|^{m-k} */
     for (int k = 0; k <= t->m; ++k) {
@@ -100,8 +128,9 @@ static int make_tgt(int kind, const double *par, tgt_t *t)
     t->kind = kind;
     if (kind == 1) { t->a = par[0]; t->b = par[1]; t->d = par[2]; t->m = 0; return !(par[0] > fabs(par[1]) && par[2] > 0); }
     if (kind == 2) {
-        t->m = (int)par[0] - 1; t->a = par[1]; t->b = par[2]; t->d = 0;
-        return !(par[0] >= 1 && par[0] == (int)par[0] && par[1] > fabs(par[2]));
+        const int integer = par[0] == (int)par[0] && par[0] <= 9;
+        t->m = integer ? (int)par[0] - 1 : -1; t->nu = (ld)par[0] - 0.5L; t->a = par[1]; t->b = par[2]; t->d = 0;
+        return !(par[0] >= 1 && par[1] > fabs(par[2]));
     }
     return 1;
 }

@@ -458,10 +458,15 @@ qm_status qm_exp_target_table(qm_target kind, const double *params, double *tabl
 {
     if (params == nullptr || table_dev == nullptr || (kind != QM_TARGET_HYPERBOLIC && kind != QM_TARGET_VG))
         return QM_EINVAL;
-    // a valid VG with lambda not an integer in [1, 9]: unsupported (lambda < 1 is out of scope)
-    if (kind == QM_TARGET_VG && params[0] > 0.0 && params[1] > std::fabs(params[2]) &&
-        (params[0] != std::floor(params[0]) || params[0] < 1.0 || params[0] > QM_RODE_VG_MAXM + 1))
-        return QM_EUNSUPPORTED;
+    // a valid VG (lambda > 0, alpha > |beta|) outside the supported lambda range:
+    // lambda < 1 is out of scope (H(0) diverges), 1 < lambda < 1.1 needs the
+    // "many steps near v = 0" P:395 warns of, and lambda > 30 is untested
+    if (kind == QM_TARGET_VG && params[0] > 0.0 && params[1] > std::fabs(params[2])) {
+        const double lam = params[0];
+        const bool integer = lam == std::floor(lam);
+        if (lam < 1.0 || lam > QM_RODE_VG_LAMBDA_MAX || (!integer && lam < QM_RODE_VG_LAMBDA_MIN_REAL))
+            return QM_EUNSUPPORTED;
+    }
     static_assert(QM_RODE_TABLE_DOUBLES == QM_RODE_TABLE_LEN, "qm.h and qm_rode_params.h disagree");
     std::vector<double> tab(QM_RODE_TABLE_DOUBLES);
     if (!rode_table_build((int)kind, params, tab.data())) return QM_EINVAL;

@@ -1,6 +1,11 @@
 // qm_rode_host.cpp -- per-parameter host setup of the exponential-base
 // recycling maps of §4: hyperbolic (§4.1) and
-// variance gamma with integer lambda (§4.2; reading R25).
+// variance gamma with real lambda >= 1 (§4.2; "if lambda > 1 matters
+// remain reasonably straightforward ... The recycling ODE may be solved as
+// before").  VG density e^{bx} |x|^nu K_nu(a|x|), nu = lambda - 1/2:
+// integer lambda <= 9 by the half-integer closed form of K (A&S 10.2.15), any
+// other lambda by K_nu of real order (Temme's series for x <= 2, Steed's
+// continued fraction CF2 beyond, forward recurrence in the order; reading R29).
 //
 // The map Q solves the Recycling ODE with an exponential base (P:104-114,
 // P:330-345):   right (v > 0):  Q'' + (a-b) Q' = H(Q) Q'^2
@@ -23,6 +28,9 @@
 #include <cstring>
 #include <cstdint>
 
+extern "C" {
+#include <quadmath.h>
+}
 #include "qm_rode_params.h"
 
 namespace qm {
@@ -31,16 +39,130 @@ typedef long double ld;
 
 namespace {
 
+// ------------------------------------------------ K_nu of real order (VG)
+// e^x K_mu(x) and e^x K_{mu+1}(x) for |mu| <= 1/2, x > 0 (scaled by e^x so that
+// the far tail, x ~ 10^3, stays in range):
+//  x <= 2: Temme's series (J. Comput. Phys. 19, 1975):
+//     K_mu = sum_k c_k f_k, K_{mu+1} = (2/x) sum_k c_k (p_k - k f_k), c_k = (x^2/4)^k / k!,
+//     f_k = (k f_{k-1} + p_{k-1} + q_{k-1}) / (k^2 - mu^2), p_k = p_{k-1}/(k - mu), q_k = q_{k-1}/(k + mu),
+//     f_0 = (mu pi / sin(mu pi)) [cosh(s) G1 + (sinh(s)/s) ln(2/x) G2], s = mu ln(2/x),
+//     p_0 = (x/2)^-mu Gamma(1+mu)/2, q_0 = (x/2)^mu Gamma(1-mu)/2,
+//     G1 = (1/Gamma(1-mu) - 1/Gamma(1+mu))/(2 mu), G2 = (1/Gamma(1-mu) + 1/Gamma(1+mu))/2
+//     (G1, G2 in __float128; G1 -> -Euler gamma as mu -> 0);
+//  x > 2: Steed's algorithm for the continued fraction CF2 (Thompson & Barnett,
+//     J. Comput. Phys. 64, 1986), which gives K_mu and K_{mu+1}/K_mu together.
+struct KTemme { ld mu, gam1, gam2, gampl, gammi; };
+
+KTemme temme_setup(ld mu)
+{
+    KTemme t;
+    t.mu = mu;
+    const __float128 m = (__float128)mu;
+    const __float128 gp = 1 / tgammaq(1 + m), gm = 1 / tgammaq(1 - m);
+    t.gampl = (ld)gp;
+    t.gammi = (ld)gm;
+    t.gam2 = (ld)((gm + gp) / 2);
+    t.gam1 = (fabsq(m) < 1e-12Q) ? -0.57721566490153286060651209008240243L : (ld)((gm - gp) / (2 * m));
+    return t;
+}
+
+void bessel_k_pair_scaled(const KTemme &T, ld x, ld *kmu, ld *kmu1)
+{
+    const ld mu = T.mu, EPS = 1e-21L;
+    if (x <= 2.0L) {
+        const ld x2 = 0.5L * x, pimu = M_PIl * mu;
+        const ld fact = (fabsl(pimu) < 1e-18L) ? 1.0L : pimu / sinl(pimu);
+        ld d = -logl(x2);
+        ld e = mu * d;
+        const ld fact2 = (fabsl(e) < 1e-18L) ? 1.0L : sinhl(e) / e;
+        ld ff = fact * (T.gam1 * coshl(e) + T.gam2 * fact2 * d);
+        ld sum = ff;
+        e = expl(e);
+        ld p = 0.5L * e / T.gampl, q = 0.5L / (e * T.gammi), c = 1.0L;
+        d = x2 * x2;
+        ld sum1 = p;
+        for (int i = 1; i < 400; ++i) {
+            ff = ((ld)i * ff + p + q) / ((ld)i * (ld)i - mu * mu);
+            c *= d / (ld)i;
+            p /= ((ld)i - mu);
+            q /= ((ld)i + mu);
+            const ld del = c * ff;
+            sum += del;
+            sum1 += c * p - (ld)i * del;
+            if (fabsl(del) < fabsl(sum) * EPS) break;
+        }
+        const ld ex = expl(x);
+        *kmu = sum * ex;
+        *kmu1 = sum1 * (2.0L / x) * ex;
+        return;
+    }
+    ld b = 2.0L * (1.0L + x), d = 1.0L / b, h = d, delh = d, q1 = 0.0L, q2 = 1.0L;
+    const ld a1 = 0.25L - mu * mu;
+    ld q = a1, c = a1, a = -a1, s = 1.0L + q * delh;
+    for (int i = 2; i < 100000; ++i) {
+        a -= 2.0L * (ld)(i - 1);
+        c = -a * c / (ld)i;
+        const ld qnew = (q1 - b * q2) / a;
+        q1 = q2;
+        q2 = qnew;
+        q += c * qnew;
+        b += 2.0L;
+        d = 1.0L / (b + a * d);
+        delh = (b * d - 1.0L) * delh;
+        h += delh;
+        const ld dels = q * delh;
+        s += dels;
+        if (fabsl(dels / s) < EPS) break;
+    }
+    h = a1 * h;
+    *kmu = sqrtl(M_PIl / (2.0L * x)) / s;
+    *kmu1 = *kmu * (mu + x + 0.5L - h) / x;
+}
+
+// e^x K_{nu-1}(x) and e^x K_nu(x) for nu >= 1/2 (forward recurrence from mu = nu - round(nu))
+struct KReal {
+    ld nu = 0.5L;
+    int nl = 1;
+    KTemme T{};
+    void setup(ld nu_)
+    {
+        nu = nu_;
+        nl = (int)(nu_ + 0.5L);
+        T = temme_setup(nu_ - (ld)nl);
+    }
+    void pair(ld x, ld *km1, ld *k) const
+    {
+        ld a, b;                                             // (K_{mu+j}, K_{mu+j+1})
+        bessel_k_pair_scaled(T, x, &a, &b);
+        for (int j = 0; j < nl - 1; ++j) {
+            const ld nx = 2.0L * (T.mu + (ld)(j + 1)) / x * b + a;
+            a = b;
+            b = nx;
+        }
+        *km1 = a;
+        *k = b;
+    }
+};
+
 struct Target {
     int kind;            // QM_RODE_HYPERBOLIC / QM_RODE_VG
     ld a, b, d;          // alpha, beta, delta (delta unused for VG)
-    int m;               // VG: lambda - 1
+    int m;               // VG with integer lambda <= 9: lambda - 1; -1: real lambda (Bessel path)
     ld c[QM_RODE_VG_MAXM + 1];   // VG: polynomial coefficients of S(|x|)
+    ld nu = 0.5L, log_f0 = 0.0L; // VG real lambda: nu = lambda - 1/2, log of the x -> 0 limit of |x|^nu K_nu(a|x|)
+    KReal K;
 
     // log of the unnormalised density
     ld logg(ld x) const
     {
         if (kind == QM_RODE_HYPERBOLIC) return -a * sqrtl(d * d + x * x) + b * x;
+        if (m < 0) {                                         // e^{bx} |x|^nu K_nu(a|x|)
+            const ld ax = fabsl(x);
+            if (ax == 0.0L) return log_f0;
+            ld km1, k;
+            K.pair(a * ax, &km1, &k);
+            return b * x + nu * logl(ax) + logl(k) - a * ax;
+        }
         const ld ax = fabsl(x);
         ld s = c[m];
         for (int k = m - 1; k >= 0; --k) s = s * ax + c[k];          // S(|x|) = sum c_j |x|^j
@@ -51,6 +173,13 @@ struct Target {
     ld H(ld x, int dir) const
     {
         if (kind == QM_RODE_HYPERBOLIC) return a * x / sqrtl(d * d + x * x) - b;
+        if (m < 0) {   // -(log f)' = -b + sign a K_{nu-1}(a|x|)/K_nu(a|x|); the ratio -> 0 at x = 0 (nu > 1/2)
+            const ld ax = fabsl(x);
+            if (ax == 0.0L) return -b;
+            ld km1, k;
+            K.pair(a * ax, &km1, &k);
+            return -b + (ld)dir * a * (km1 / k);
+        }
         const ld ax = fabsl(x), sg = (ld)dir;
         ld s = c[m], ds = 0.0L;
         for (int k = m - 1; k >= 0; --k) { ds = ds * ax + s; s = s * ax + c[k]; }
@@ -81,7 +210,18 @@ ld tail_mass(const Target &t, ld x, int dir, ld rate, ld shift)
     ld w = 0.125L / rate;
     if (t.kind == QM_RODE_HYPERBOLIC && w > 0.25L * t.d) w = 0.25L * t.d;    // resolve sqrt(d^2 + x^2)
     ld s = 0.0L;
-    for (int k = 0; k < 400000; ++k) {
+    int k0 = 0;
+    if (x == 0.0L && t.kind == QM_RODE_VG && t.m < 0) {
+        // real-order VG: |x|^nu K_nu(a|x|) = A(x^2) + |x|^(2 nu) B(x^2) (+ a log for integer
+        // nu) is not smooth at 0, so the first panel is cut geometrically towards 0
+        // (each sub-panel is smooth on its own scale; 2^-64 w is below the ld floor)
+        for (int j = 64; j >= 0; --j) {
+            const ld a0 = ldexpl(w, -j - 1), a1 = ldexpl(w, -j);
+            s += (dir > 0) ? gl10(t, a0, a1, shift) : gl10(t, -a1, -a0, shift);
+        }
+        k0 = 1;
+    }
+    for (int k = k0; k < 400000; ++k) {
         const ld lo = (dir > 0) ? x + k * w : x - (k + 1) * w;
         const ld p = gl10(t, lo, lo + w, shift);
         s += p;
@@ -94,8 +234,7 @@ ld tail_mass(const Target &t, ld x, int dir, ld rate, ld shift)
 
 bool rode_table_build(int kind, const double *params, double *tab)
 {
-    Target t;
-    std::memset(&t, 0, sizeof(t));
+    Target t{};
     t.kind = kind;
     if (kind == QM_RODE_HYPERBOLIC) {
         t.a = params[0]; t.b = params[1]; t.d = params[2];
@@ -103,12 +242,20 @@ bool rode_table_build(int kind, const double *params, double *tab)
     } else if (kind == QM_RODE_VG) {
         const double lam = params[0];
         t.a = params[1]; t.b = params[2];
-        if (!(lam >= 1 && lam <= QM_RODE_VG_MAXM + 1 && lam == std::floor(lam) && t.a > 0 && fabsl(t.b) < t.a))
-            return false;
-        t.m = (int)lam - 1;
+        if (!(lam >= 1 && lam <= QM_RODE_VG_LAMBDA_MAX && t.a > 0 && fabsl(t.b) < t.a)) return false;
+        if (lam != std::floor(lam) || lam > QM_RODE_VG_MAXM + 1) {
+            if (lam < QM_RODE_VG_LAMBDA_MIN_REAL) return false;
+            t.m = -1;
+            t.nu = (ld)lam - 0.5L;
+            t.K.setup(t.nu);
+            // |x|^nu K_nu(a|x|) -> Gamma(nu) 2^(nu-1) a^-nu as x -> 0 (nu > 0)
+            t.log_f0 = lgammal(t.nu) + (t.nu - 1.0L) * logl(2.0L) - t.nu * logl(t.a);
+        } else {
+            t.m = (int)lam - 1;
+        }
         // K_{m+1/2}(z) = sqrt(pi/2z) e^-z sum_k (m+k)!/(k!(m-k)!) (2z)^-k  (A&S 10.2.15), so
         // f ~ e^{bx - a|x|} sum_k (m+k)!/(k!(m-k)!) (2a)^-k |x|^{m-k};  c[j] multiplies |x|^j
-        for (int k = 0; k <= t.m; ++k) {
+        for (int k = 0; k <= t.m; ++k) {   // (m < 0, real lambda: no polynomial)
             ld co = 1.0L;
             for (int j = t.m - k + 1; j <= t.m + k; ++j) co *= (ld)j;
             for (int j = 2; j <= k; ++j) co /= (ld)j;
@@ -191,9 +338,27 @@ bool rode_table_build(int kind, const double *params, double *tab)
         // backward: coarse, fine, then the centre (stored only down to Wc; the
         // rest of the sweep gives the checks at v = 0)
         ld Qc = 0.0L;
+        // real-order VG: H has a |Q|^(2 nu - 1) (or Q log Q) term at the origin, so the
+        // interval next to v = 0 is stepped on a geometric mesh (w_i = h0 r^-i): RK4's
+        // error there scales with the local step over the distance to 0, not with h0
+        const bool graded = (t.kind == QM_RODE_VG && t.m < 0);
+        constexpr int NG = 4800;                               // r = 1.005: h0 r^-4800 ~ 4e-11 h0 (r = 1.12 left 1e-13 at lambda = 1.5,
+                                                               // 1.02 left 5e-15 at lambda = 1.2; 1.005 converged to 1e-17 at 1.1)
+        const ld rg = 1.005L;
         for (int k = NT - 1; k >= 0; --k) {
             const ld hk = hs[seg_of(k)];
-            for (int j = 0; j < sub; ++j) rk4(Q, P, -hk / sub);
+            if (k == 0 && graded) {
+                ld w = hk;
+                for (int i = 1; i <= NG; ++i) {
+                    const ld wn = hk * powl(rg, -(ld)i);
+                    rk4(Q, P, wn - w);
+                    w = wn;
+                }
+                rk4(Q, P, -w);
+            } else {
+                const int ns = (graded && k < 64) ? sub * (64 / (k + 1)) : sub;   // finer near 0
+                for (int j = 0; j < ns; ++j) rk4(Q, P, -hk / ns);
+            }
             if (k >= Nc) put(k, Q, P);
             if (k == Nc) Qc = Q;
         }
@@ -211,7 +376,17 @@ bool rode_table_build(int kind, const double *params, double *tab)
         cQ = cP = 0.0L;
         put(0, Q, P);
         for (int k = 1; k <= Nc; ++k) {
-            for (int j = 0; j < sub; ++j) rk4(Q, P, hs[0] / sub);
+            if (k == 1 && graded) {
+                ld w = 0.0L;
+                for (int i = NG; i >= 0; --i) {
+                    const ld wn = hs[0] * powl(rg, -(ld)i);
+                    rk4(Q, P, wn - w);
+                    w = wn;
+                }
+            } else {
+                const int ns = (graded && k <= 64) ? sub * (64 / k) : sub;    // interval [k-1, k]: finer near 0
+                for (int j = 0; j < ns; ++j) rk4(Q, P, hs[0] / ns);
+            }
             if (k < Nc) put(k, Q, P);
         }
         tab[22 + side] = (double)(Q - Qc);                     // joint mismatch at Wc

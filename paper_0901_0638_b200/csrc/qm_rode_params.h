@@ -32,7 +32,9 @@
 #define QM_RODE_VRATE2 800.0
 #define QM_RODE_HEADER 80
 #define QM_RODE_SEG 32
-#define QM_RODE_VG_MAXM 8
+#define QM_RODE_VG_MAXM 8                 // integer lambda <= QM_RODE_VG_MAXM + 1: closed-form K_{m+1/2}
+#define QM_RODE_VG_LAMBDA_MIN_REAL 1.1    // non-integer lambda: K_nu of real order, lambda in [1.1, 30]
+#define QM_RODE_VG_LAMBDA_MAX 30.0
 #define QM_RODE_TABLE_LEN (QM_RODE_HEADER + 8 * (QM_RODE_NT + 1))
 
 namespace qm {

@@ -213,19 +213,16 @@ k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64
         fence_mbar_init();
     }
     __syncthreads();
-    if (warp == 0) {
-        if (lane == 0) {
-            int st = 0;
-            uint32_t ph = 0;
-            int64_t k = 0;
-            for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
-                for (int i = 0; i < TPC; ++i, ++k) {
-                    if (k >= S) mbar_wait(&empty[st], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[st], TILE_BYTES);
-                    bulk_g2s(tiles + (size_t)st * TV, z2 + (c * TPC + i) * TV, TILE_BYTES, &full[st]);
-                    if (++st == S) { st = 0; ph ^= 1; }
-                }
-        }
+    if (warp == 0) {   // producer: all lanes, one elected lane issues (qm_tma.cuh)
+        int st = 0;
+        uint32_t ph = 0;
+        int64_t k = 0;
+        for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x)
+            for (int i = 0; i < TPC; ++i, ++k) {
+                if (k >= S) mbar_wait(&empty[st], ph ^ 1);
+                elect_tma_load(&full[st], tiles + (size_t)st * TV, z2 + (c * TPC + i) * TV, TILE_BYTES);
+                if (++st == S) { st = 0; ph ^= 1; }
+            }
         return;
     }
     const int w = warp - 1;

@@ -57,6 +57,20 @@ QM_DEV void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// The producer's per-tile issue, run by ALL 32 lanes of the producer warp: one
+// lane chosen by elect.sync arms the stage's "full" barrier with the byte count
+// and issues the bulk copy, both predicated inside one asm block -- no branch, so
+// the producer contributes no divergent branch (P:551's argument, measured by ncu).
+QM_DEV void elect_tma_load(uint64_t *bar, void *dst_smem, const void *src, uint32_t bytes)
+{
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %3;\n\t"
+        "@P cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%2], %3, [%0];\n\t}"
+        :: "r"(smem_u32(bar)), "r"(smem_u32(dst_smem)), "l"(src), "r"(bytes) : "memory");
+}
+
 QM_DEV void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes)
 {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
@@ -87,17 +101,14 @@ __device__ __forceinline__ void tma_stream_map(const T *__restrict__ in, T *__re
 
     const int64_t first = blockIdx.x, step = gridDim.x;
     if (warp == 0) {
-        // ---------------- producer
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            int64_t k = 0;
-            for (int64_t t = first; t < ntiles; t += step, ++k) {
-                if (k >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], TILE_BYTES);
-                bulk_g2s(tiles + (size_t)s * TILE_ELEMS, in + t * TILE_ELEMS, TILE_BYTES, &full[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-            }
+        // ---------------- producer (all lanes; one elected lane issues)
+        int s = 0;
+        uint32_t ph = 0;
+        int64_t k = 0;
+        for (int64_t t = first; t < ntiles; t += step, ++k) {
+            if (k >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+            elect_tma_load(&full[s], tiles + (size_t)s * TILE_ELEMS, in + t * TILE_ELEMS, TILE_BYTES);
+            if (++s == STAGES) { s = 0; ph ^= 1; }
         }
     } else {
         // ---------------- consumers
@@ -166,17 +177,14 @@ __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__rest
     __syncthreads();
 
     const int64_t first = blockIdx.x, step = gridDim.x;
-    if (warp == 0) {
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            int64_t k = 0;
-            for (int64_t t = first; t < ntiles; t += step, ++k) {
-                if (k >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], TILE_BYTES);
-                bulk_g2s(tiles + (size_t)s * TILE_VECS, in + t * TILE_VECS, TILE_BYTES, &full[s]);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-            }
+    if (warp == 0) {   // producer: all 32 lanes run the loop, one elected lane issues (no divergence)
+        int s = 0;
+        uint32_t ph = 0;
+        int64_t k = 0;
+        for (int64_t t = first; t < ntiles; t += step, ++k) {
+            if (k >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+            elect_tma_load(&full[s], tiles + (size_t)s * TILE_VECS, in + t * TILE_VECS, TILE_BYTES);
+            if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         return;
     }

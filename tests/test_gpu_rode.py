@@ -1,7 +1,8 @@
 """GPU parity of the exponential-base recycling into hyperbolic / VG samples
 (SURVEY §8 row f1): the kernel (quintic Hermite on the RODE table) against the
 oracle's exact map Q(v) = F^-1(F0(v)).  Bar: 1e-14 relative in fp64 (table ~1e-16
-+ quintic interpolation on a segment grid ~3e-16; measured by emulation), 2 ulp in fp32."""
++ quintic interpolation on a segment grid ~3e-16; measured by emulation), 2 ulp in fp32.
+VG covers integer lambda (half-integer Bessel orders) and real lambda in [1.1, 30]."""
 import numpy as np
 import pytest
 import torch
@@ -13,7 +14,9 @@ pytestmark = pytest.mark.gpu
 Q = pytest.importorskip("paper_0901_0638_b200.qm")
 
 CASES = [(O.HYPERBOLIC, [1.0, 0.0, 1.0]), (O.HYPERBOLIC, [1.0, 0.5, 1.0]), (O.HYPERBOLIC, [2.0, -1.0, 0.5]),
-         (O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4])]
+         (O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4]),
+         # real lambda (K_nu of non-half-integer order; "if lambda > 1 ... solved as before")
+         (O.VG, [1.5, 2.0, 0.5]), (O.VG, [2.7, 1.0, -0.6]), (O.VG, [1.1, 1.0, 0.3])]
 
 
 def _base_samples(kind, par, n, seed=5):
@@ -34,7 +37,8 @@ def test_recycle_exp_to_target_vs_exact_map(kind, par):
     # base samples, the centre, both segment joints (base probability e^-40) and the
     # far tail out to e^-740 (the smallest double uniform gives e^-744)
     far = [1e-12, -1e-9, 40 / rr, -40 / rl, 40 / rr * (1 + 1e-9), 60.0, -70.0, 300 / rr, -500 / rl, 740 / rr, -740 / rl]
-    v = np.concatenate([_base_samples(kind, par, 400), [0.0, -0.0], far])
+    real_lambda = kind == O.VG and par[0] != int(par[0])           # slower oracle (quadrature of K_nu)
+    v = np.concatenate([_base_samples(kind, par, 120 if real_lambda else 400), [0.0, -0.0], far])
     fn = Q.qm_recycle_exp_to_hyperbolic if kind == O.HYPERBOLIC else Q.qm_recycle_exp_to_vg
     g = fn(torch.from_numpy(v).cuda(), tab).cpu().numpy()
     ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
@@ -114,3 +118,15 @@ def test_base_quantile_and_moments():
     var = mp.quad(lambda t: t * t * f(t), [-mp.inf, 0, mp.inf]) / Z - mean ** 2
     se = float(mp.sqrt(var / (1 << 24)))
     assert abs(float(x.mean()) - float(mean)) < 6 * se
+
+
+def test_vg_lambda_range():
+    """lambda < 1 is out of scope, 1 < lambda < 1.1 unsupported (the near-origin
+    behaviour P:395 warns of); real lambda in [1.1, 30] builds."""
+    for lam in (0.5, 1.05, 31.0):
+        with pytest.raises(Q.QMError) as e:
+            Q.qm_exp_target_table(O.VG, [lam, 2.0, 0.5])
+        assert e.value.status == 2
+    with pytest.raises(Q.QMError) as e:
+        Q.qm_exp_target_table(O.VG, [2.5, 1.0, 1.5])              # |beta| >= alpha
+    assert e.value.status == 1

@@ -105,7 +105,8 @@ def test_vg_lambda2_closed_form_cdf():
 
 # ------------------------------------------- the product's host-side table builder
 @pytest.mark.parametrize("kind,par", [(O.HYPERBOLIC, p) for p in HYP] +
-                         [(O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4])])
+                         [(O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4]),
+                          (O.VG, [1.5, 2.0, 0.5]), (O.VG, [2.7, 1.0, -0.6])])
 def test_product_rode_table_vs_oracle(kind, par):
     """libqm's table (RODE integrated backward in long double, the centre segment
     forward) at sampled nodes of each segment vs the oracle's exact map, R' and R''
@@ -140,3 +141,75 @@ def test_product_rode_table_vs_oracle(kind, par):
         d2 = ((qp - 2 * q0 + qm) / np.longdouble(hh) ** 2).astype(np.float64)
         assert np.abs(d1 / nodes[ks, 1] - 1).max() < 1e-7
         assert np.abs(d2 - nodes[ks, 2]).max() < 1e-6 * (1 + np.abs(nodes[ks, 2]).max())
+
+
+# ------------------------------------------- VG with real lambda > 1 (reading R29)
+def _mp_lam(lam):
+    return mp.mpf(float(lam))          # the double the oracle receives, exactly
+
+
+@pytest.mark.parametrize("nu,z", [(0.6, 3.0), (1.0, 0.5), (2.2, 1e-3), (2.2, 1.0), (3.0, 2.0), (5.5, 30.0),
+                                  (7.3, 1e-5), (2.2, 500.0), (4.75, 12.0)])
+def test_besselk_trapezoid_vs_mpmath(nu, z):
+    """The oracle's K_nu (trapezoidal rule on A&S 9.6.24) vs mpmath besselk."""
+    mp.mp.dps = 40
+    rel = abs(ld2mp(O.besselk(nu, z)) / mp.besselk(nu, z) - 1)
+    assert rel < (2e-17 if z < 100 else 1e-16), rel
+
+
+@pytest.mark.parametrize("m", [0, 1, 2, 4])
+def test_besselk_half_integer_closed_form(m):
+    """K_{m+1/2}(z) = sqrt(pi/2z) e^-z sum_k (m+k)!/(k!(m-k)!) (2z)^-k (A&S 10.2.15), the
+    form the oracle uses for integer lambda: the two VG paths describe one density."""
+    mp.mp.dps = 40
+    for z in (0.05, 1.0, 7.5):
+        cf = mp.sqrt(mp.pi / (2 * z)) * mp.exp(-z) * mp.fsum(
+            mp.factorial(m + k) / (mp.factorial(k) * mp.factorial(m - k)) * (2 * mp.mpf(z)) ** (-k) for k in range(m + 1))
+        assert abs(ld2mp(O.besselk(m + 0.5, z)) / cf - 1) < 2e-17
+
+
+def _vg_masses_2f1(lam, a, b):
+    """p+ and p- as printed in P:372-393 (A&S/G&R 6.621.3), mpmath hyp2f1."""
+    L = _mp_lam(lam)
+    a, b = mp.mpf(a), mp.mpf(b)
+    pre = 2 ** (2 * L - 1) * mp.gamma(L + mp.mpf(1) / 2) / (mp.sqrt(mp.pi) * mp.gamma(L + 1))
+    pp = pre * ((a + b) / (a - b)) ** L * mp.hyp2f1(2 * L, L, L + 1, (a + b) / (b - a))
+    pm = pre * ((a - b) / (a + b)) ** L * mp.hyp2f1(2 * L, L, L + 1, (b - a) / (a + b))
+    return pm, pp
+
+
+@pytest.mark.parametrize("lam,a,b", [(2, 2.0, 0.5), (3, 1.0, -0.4), (1.5, 2.0, 0.5), (2.7, 2.0, 0.5),
+                                     (2.7, 1.0, -0.6), (3.3, 1.5, 0.2), (5.25, 2.0, 1.2), (1.2, 1.0, 0.3)])
+def test_vg_masses_vs_printed_2f1(lam, a, b):
+    """p+- of the oracle (quadrature of the density) vs the paper's closed forms
+    (P:372-393), and vs the regularized incomplete beta I_{(a+b)/2a}(lambda, lambda)
+    (VG = difference of two Gamma(lambda) variables with rates a-b and a+b)."""
+    mp.mp.dps = 50
+    m = O.target_masses(O.VG, [lam, a, b])
+    pm, pp = _vg_masses_2f1(lam, a, b)
+    assert abs(pp + pm - 1) < mp.mpf(10) ** -40
+    assert abs(ld2mp(m[1]) - pp) < 2e-17 and abs(ld2mp(m[0]) - pm) < 2e-17, (ld2mp(m[1]) - pp)
+    ib = mp.betainc(_mp_lam(lam), _mp_lam(lam), 0, (mp.mpf(a) + b) / (2 * mp.mpf(a)), regularized=True)
+    assert abs(ib - pp) < mp.mpf(10) ** -40
+    if b == 0:
+        assert abs(ld2mp(m[1]) - mp.mpf(1) / 2) < 1e-18
+
+
+@pytest.mark.parametrize("par", [[1.5, 2.0, 0.5], [2.7, 1.0, -0.6], [1.2, 1.0, 0.3]])
+def test_vg_real_lambda_map_vs_mpmath(par):
+    """Q(v) = F^-1(F0(v)) for real lambda (K_nu of non-half-integer order): the tail
+    mass beyond Q equals the base's, by mpmath quadrature of the printed density."""
+    mp.mp.dps = 24
+    lam, a, b = _mp_lam(par[0]), mp.mpf(par[1]), mp.mpf(par[2])
+    f = lambda x: mp.exp(b * x) * abs(x) ** (lam - mp.mpf(1) / 2) * mp.besselk(lam - mp.mpf(1) / 2, a * abs(x))
+    Z = mp.quad(f, [-mp.inf, -1, 0, 1, mp.inf])
+    pm, pp = _vg_masses_2f1(par[0], par[1], par[2])
+    v = np.array([0.05, 7.0, -0.3, -4.0])
+    q = O.recycle_exp_to_target(O.VG, par, v)
+    for vi, qi in zip(v, q):
+        qq = ld2mp(qi)
+        if vi > 0:
+            lhs, rhs = mp.quad(f, [qq, qq + 1, mp.inf]) / Z, pp * mp.exp(-(a - b) * vi)
+        else:
+            lhs, rhs = mp.quad(f, [-mp.inf, qq - 1, qq]) / Z, pm * mp.exp((a + b) * vi)
+        assert abs(lhs - rhs) / (f(qq) / Z) <= 1e-16 * max(1, abs(qq)), (vi, lhs - rhs)
