@@ -95,6 +95,15 @@ int         qm_device_sm_count(void);
 qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p,
                              qm_algorithm alg, void *stream);
 
+/* Config 1 like-for-like (Table 3): the same formulas in PLAIN double,
+ * as the paper's codes are written -- FMA Horner, library log/sqrt/erfc/exp, IEEE
+ * division, per-element branches, no compensation.  fp64 only; alg in
+ * {QM_BREAKLESS (App D), QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED,
+ * QM_MORO}, else QM_EUNSUPPORTED.  Same element semantics as qm_normal_quantile;
+ * accuracy that of plain double evaluation (not the 2-ulp contract): a timing
+ * comparison, not a product path. */
+qm_status qm_normal_quantile_plain(const void *u, void *z, int64_t n, qm_algorithm alg, void *stream);
+
 /* Antithetic pairs ("always work antithetically"): for each
  * u[i] in (0,1]: v = -log u[i] ("better, v = -log[u]"), Z = Q(v) >= 0,
  * z_pairs[2i] = Z, z_pairs[2i+1] = -Z.  2n outputs.  u = 0 -> {+inf, -inf};

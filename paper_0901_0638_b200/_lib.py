@@ -38,6 +38,7 @@ SIGNATURES = {
     "qm_device_sm_count": (_I32, []),
     "qm_normal_quantile": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
     "qm_normal_antithetic": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
+    "qm_normal_quantile_plain": (_I32, [_P, _P, _I64, _I32, _P]),
     "qm_philox_uniform": (_I32, [_P, _I64, _I32, _U64, _U64, _P]),
     "qm_normal_philox": (_I32, [_P, _I64, _I32, _I32, _U64, _U64, _P]),
     "qm_recycle_normal_to_t": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P]),

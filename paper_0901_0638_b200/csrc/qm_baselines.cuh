@@ -138,6 +138,116 @@ QM_DEV double moro(double u)
     return (yd < 0.0) ? -xr : xr;
 }
 
+// ------------------------------------------------------------------------
+// Plain-double versions (config 1 like-for-like with the paper's Table 3, whose
+// codes are all plain double: "Acklam single coded as double", Lea's refined
+// Acklam, App D, AS241 -- P:634-662): the same formulas and region breaks,
+// every operation one IEEE double operation (FMA Horner, CUDA log/sqrt/erfc/exp,
+// IEEE division), no compensation.  Their accuracy is that of plain double
+// evaluation (bounded by ~(2 N + 3) ulp for N-term polynomials; measured by the
+// tests), not the 2-ulp contract of the kernels above.
+template <int N>
+QM_DEV double horner_plain(const double *a, double x)
+{
+    double s = a[N - 1];
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) s = __fma_rn(s, x, a[i]);
+    return s;
+}
+
+QM_DEV double specials_or(double u, double x)
+{
+    x = (u == 0.0) ? -inf_d() : x;
+    x = (u == 1.0) ? inf_d() : x;
+    return (u >= 0.0 && u <= 1.0) ? x : nan_d();
+}
+
+// App D and the (7,7) of App A, as printed: vv, z = -log(2 vv), z P(z)/Q(z), sign
+template <int ALG>
+QM_DEV double breakless_plain(double u)
+{
+    const double omu = 1.0 - u;
+    const double vv = fmin(u, omu);
+    const double z = -log(2.0 * vv);
+    const double r = (ALG == ALG_BREAKLESS77) ? z * horner_plain<8>(kA77P_d, z) / horner_plain<8>(kA77Q_d, z)
+                                              : z * horner_plain<14>(kD13P, z) / horner_plain<14>(kD13Q, z);
+    return specials_or(u, (u < 0.5) ? -r : r);
+}
+
+QM_DEV double as241_plain(double u)
+{
+    const double q = u - 0.5;
+    double x;
+    if (fabs(q) <= 0.425) {
+        const double r = 0.180625 - q * q;
+        x = q * horner_plain<8>(kAS_A, r) / horner_plain<8>(kAS_B, r);
+    } else {
+        const double t = (q < 0.0) ? u : 1.0 - u;
+        double r = sqrt(-log(t));
+        if (r <= 5.0) {
+            r -= 1.6;
+            x = horner_plain<8>(kAS_C, r) / horner_plain<8>(kAS_D, r);
+        } else {
+            r -= 5.0;
+            x = horner_plain<8>(kAS_E, r) / horner_plain<8>(kAS_F, r);
+        }
+        x = (q < 0.0) ? -x : x;
+    }
+    return specials_or(u, x);
+}
+
+template <bool REFINE>
+QM_DEV double acklam_plain(double p)
+{
+    const double t = (p < 0.5) ? p : 1.0 - p;
+    double x;
+    if (t < 0.02425) {
+        const double q = sqrt(-2.0 * log(t));
+        x = horner_plain<6>(kAK_C, q) / horner_plain<5>(kAK_D, q);
+    } else {
+        const double q = t - 0.5, r = q * q;
+        x = q * horner_plain<6>(kAK_A, r) / horner_plain<6>(kAK_B, r);
+    }
+    if (REFINE && t >= 2.2250738585072014e-308) {
+        const double e = 0.5 * erfc(-x * 0.70710678118654752440) - t;
+        const double uu = e * 2.50662827463100050242 * exp(0.5 * x * x);
+        x = x - uu / (1.0 + 0.5 * x * uu);
+    }
+    return specials_or(p, (p < 0.5) ? x : -x);
+}
+
+QM_DEV double moro_plain(double u)
+{
+    const double y = u - 0.5;
+    double x;
+    if (fabs(y) < 0.42) {
+        const double r = y * y;
+        x = y * horner_plain<4>(kMO_A, r) / horner_plain<5>(kMO_B, r);
+    } else {
+        const double t = (y < 0.0) ? u : 1.0 - u;
+        x = horner_plain<9>(kMO_C, log(-log(t)));
+        x = (y < 0.0) ? -x : x;
+    }
+    return specials_or(u, x);
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(256)
+k_plain_f64(const double *__restrict__ u, double *__restrict__ z, int64_t n)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double x = u[i];
+        double r;
+        if (ALG == ALG_BREAKLESS || ALG == ALG_BREAKLESS77) r = breakless_plain<ALG>(x);
+        else if (ALG == ALG_AS241) r = as241_plain(x);
+        else if (ALG == ALG_ACKLAM) r = acklam_plain<false>(x);
+        else if (ALG == ALG_ACKLAM_REF) r = acklam_plain<true>(x);
+        else r = moro_plain(x);
+        z[i] = r;
+    }
+}
+
 template <int ALG>
 QM_DEV double branchy(double u)
 {

@@ -285,6 +285,26 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
     });
 }
 
+qm_status qm_normal_quantile_plain(const void *u, void *z, int64_t n, qm_algorithm alg, void *stream)
+{
+    if (n < 0 || bad_ptrs(u, z, n) || alg < QM_BREAKLESS || alg > QM_ALG_LAST) return QM_EINVAL;
+    if (n == 0) return QM_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const double *ud = (const double *)u;
+    double *zd = (double *)z;
+    const int g = grid_for(n, kThreads, 8);
+    switch (alg) {
+    case QM_BREAKLESS: k_plain_f64<ALG_BREAKLESS><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    case QM_BREAKLESS77: k_plain_f64<ALG_BREAKLESS77><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    case QM_AS241: k_plain_f64<ALG_AS241><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    case QM_ACKLAM: k_plain_f64<ALG_ACKLAM><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    case QM_ACKLAM_REFINED: k_plain_f64<ALG_ACKLAM_REF><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    case QM_MORO: k_plain_f64<ALG_MORO><<<g, kThreads, 0, s>>>(ud, zd, n); break;
+    default: return QM_EUNSUPPORTED;
+    }
+    return launched();
+}
+
 qm_status qm_normal_antithetic(const void *u, void *z, int64_t n, qm_precision p, qm_algorithm alg, void *stream)
 {
     if (n < 0 || bad_ptrs(u, z, n)) return QM_EINVAL;

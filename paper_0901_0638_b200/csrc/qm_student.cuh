@@ -208,8 +208,8 @@ k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64
     double2 *t2 = reinterpret_cast<double2 *>(t);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NC); }
+    if (warp == 0) {
+        for (int i = 0; i < S; ++i) { mbar_init_elect(&full[i], 1); mbar_init_elect(&empty[i], NC); }
         fence_mbar_init();
     }
     __syncthreads();
@@ -266,12 +266,15 @@ k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64
             s3 = __dadd_rn(s3, __shfl_xor_sync(0xffffffffu, s3, d));
             s4 = __dadd_rn(s4, __shfl_xor_sync(0xffffffffu, s4, d));
         }
-        if (lane == 0) { part[w][0] = s1; part[w][1] = s2; part[w][2] = s3; part[w][3] = s4; }
+        // every lane holds the warp totals: lane l stores column l & 3 (8 lanes store
+        // the same value to each address) -- no lane-dependent branch
+        const int col = lane & 3;
+        part[w][col] = (col == 0) ? s1 : (col == 1) ? s2 : (col == 2) ? s3 : s4;
         consumer_bar(NC * 32);
-        if (w == 0 && lane < 4) {
+        if (w == 0) {                                               // warp-uniform
             double r = 0.0;
-            for (int q = 0; q < NC; ++q) r = __dadd_rn(r, part[q][lane]);
-            rows[c * 4 + lane] = r;
+            for (int q = 0; q < NC; ++q) r = __dadd_rn(r, part[q][col]);
+            rows[c * 4 + col] = r;                                  // same value from 8 lanes
         }
         consumer_bar(NC * 32);                                      // part[] reused by the next chunk
     }

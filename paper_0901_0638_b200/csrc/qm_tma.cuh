@@ -32,6 +32,14 @@ QM_DEV void mbar_init(uint64_t *bar, uint32_t count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
 }
+// called by a whole warp: one elected lane initialises the barrier (predicated,
+// no branch -- the kernels then have no divergent branch at all)
+QM_DEV void mbar_init_elect(uint64_t *bar, uint32_t count)
+{
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\t"
+                 "@P mbarrier.init.shared::cta.b64 [%0], %1;\n\t}"
+                 :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
 QM_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 QM_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -93,8 +101,8 @@ __device__ __forceinline__ void tma_stream_map(const T *__restrict__ in, T *__re
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    if (warp == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init_elect(&full[s], 1); mbar_init_elect(&empty[s], 1); }
         fence_mbar_init();
     }
     __syncthreads();
@@ -170,8 +178,8 @@ __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__rest
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC); }
+    if (warp == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init_elect(&full[s], 1); mbar_init_elect(&empty[s], NC); }
         fence_mbar_init();
     }
     __syncthreads();

@@ -81,6 +81,17 @@ def qm_normal_quantile(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=N
     return z
 
 
+def qm_normal_quantile_plain(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
+    """Plain-double version of the formula (config 1 like-for-like timing, Table 3)."""
+    _dev(u, "u")
+    if u.dtype != torch.float64:
+        raise ValueError("qm_normal_quantile_plain is fp64 only")
+    z = _out(u, out)
+    L.check("qm_normal_quantile_plain", L.load().qm_normal_quantile_plain(
+        u.data_ptr(), z.data_ptr(), u.numel(), alg, _stream(stream)))
+    return z
+
+
 def qm_normal_antithetic(u: torch.Tensor, out=None, alg: int = BREAKLESS, stream=None) -> torch.Tensor:
     _dev(u, "u")
     z = _out(u, out, 2 * u.numel())

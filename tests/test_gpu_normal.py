@@ -189,6 +189,37 @@ def test_refined_acklam():
     assert np.array_equal(np.isnan(g), np.isnan(ref.astype(np.float64)))
 
 
+# ------------------------- config 1 like-for-like: plain double
+@pytest.mark.parametrize("alg,name,nterms", [(Q.BREAKLESS, "d13", 14), (Q.BREAKLESS77, "a77", 8), (Q.AS241, "as241", 8),
+                                             (Q.ACKLAM, "acklam", 6), (Q.MORO, "moro", 9)])
+def test_plain_double_versions(alg, name, nterms):
+    """qm_normal_quantile_plain: the same formulas coded in plain double like the
+    paper's Table 3 programs.  Bar: the plain-evaluation bound (2 N + 5) ulp of the
+    same formula (N = terms of the longer polynomial; 2N roundings of two Horner
+    chains, + log/sqrt, division and the final product); tail-stratified inputs
+    exercise every region."""
+    u = np.concatenate([I.tail_stratified((1 << 18) + 11, dtype=np.float64), I.mixed_uniforms(1 << 16, dtype=np.float64)])
+    g = _gpu(Q.qm_normal_quantile_plain, u, alg=alg)
+    ref = {"d13": lambda: O.normal_breakless(u, O.D13, 64), "a77": lambda: O.normal_breakless(u, O.A77, 64),
+           "as241": lambda: O.normal_as241(u, 64), "acklam": lambda: O.normal_acklam(u, 64, False),
+           "moro": lambda: O.normal_moro(u, 64)}[name]()
+    err = ulp_errors(g, ref, np.float64)
+    print(name, "plain max ulp", summary(err))
+    assert err.max() <= 2 * nterms + 5, summary(err)
+
+
+def test_plain_refined_acklam():
+    u = I.tail_stratified((1 << 18) + 11, dtype=np.float64)
+    g = _gpu(Q.qm_normal_quantile_plain, u, alg=Q.ACKLAM_REFINED)
+    ref = O.normal_acklam(u, 64, True)
+    fin = np.isfinite(ref)
+    r = ref[fin].astype(np.float64)
+    t = np.minimum(u[fin], 1 - u[fin])
+    phi = np.exp(-0.5 * r * r) / np.sqrt(2 * np.pi)
+    tol = 4 * np.spacing(np.abs(r)) + 8 * np.finfo(np.float64).eps * t / phi
+    assert np.all(np.abs(g[fin] - r) <= tol)
+
+
 # --------------------------------------- full size, bench launch configuration
 def test_full_size_streaming_sampled():
     """configs[1]: 2^28 fp32 uniforms in HBM -> breakless quantile (the bench.py

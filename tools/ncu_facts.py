@@ -11,7 +11,11 @@ import sys
 # elements per captured launch (tools/prof_kernel.py)
 ELEMS = {"stream_f32": 1 << 28, "stream_f32_ldg": 1 << 28, "stream_f64": 1 << 28, "fused_f32": 1 << 32,
          "fused_f64": 1 << 31, "student": 1 << 30, "exp2n_f32": 1 << 28, "moments": 1 << 30, "mc": 1 << 32,
-         "student_moments": 1 << 30, "two_region": 1 << 28, "rode_hyp_f64": 1 << 28, "rode_philox_f32": 1 << 28}
+         "student_moments": 1 << 30, "two_region": 1 << 28, "rode_hyp_f64": 1 << 28, "rode_philox_f32": 1 << 28,
+         "stream_f64_1212": 1 << 28, "fused_f32_fma": 1 << 32}
+for _a in ("breakless", "as241", "acklam", "refined", "moro"):      # config 1: one launch of 2^20
+    ELEMS[f"config1_{_a}"] = 1 << 20
+    ELEMS[f"plain_config1_{_a}"] = 1 << 20
 
 d = sys.argv[1]
 out = {}
@@ -23,6 +27,11 @@ for name, n in ELEMS.items():
     out[name] = {"kernel": k["kernel"],
                  "dram_bytes_per_elem": (k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0)) / n,
                  "warp_inst_per_elem": k.get("warp_inst_executed", 0) / n,
+                 "fp64_inst_per_elem": k.get("fp64_inst_executed", 0) / n,
                  "source": f"{p} (ncu --set full, one launch of {n} samples)"}
+    for key in ("fp64_pipe_pct", "fma_pipe_pct", "alu_pipe_pct", "xu_pipe_pct", "issue_active_pct",
+                "divergent_branch_targets", "threads_per_inst", "registers"):
+        if key in k:
+            out[name][key] = k[key]
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
 print(json.dumps(out, indent=1))

@@ -25,6 +25,8 @@ KEYS = {
     "divergent_branch_targets": "smsp__sass_branch_targets_threads_divergent.sum",
     "threads_per_inst": "smsp__thread_inst_executed_per_inst_executed.ratio",
     "warp_inst_executed": "smsp__inst_executed.sum",
+    "fp64_inst_executed": "smsp__inst_executed_pipe_fp64.sum",
+    "fma_cycles_active": "sm__pipe_fma_cycles_active.sum",
     "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
     "grid": "launch__grid_size",
     "block": "launch__block_size",

@@ -16,24 +16,26 @@ if name in ("stream_f32", "stream_f32_two"):
     z = torch.empty_like(u)
     alg = Q.TWO_REGION if name == "stream_f32_two" else Q.BREAKLESS
     fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
-elif name == "stream_f64":
+elif name in ("stream_f64", "stream_f64_1212"):
     u = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
     z = torch.empty_like(u)
-    fn = lambda: Q.qm_normal_quantile(u, out=z)
+    alg = Q.BREAKLESS1212 if name == "stream_f64_1212" else Q.BREAKLESS
+    fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
 elif name == "fused_f32":
     z = torch.empty(1 << 32, dtype=torch.float32, device="cuda")
     fn = lambda: Q.qm_normal_philox(1 << 32, SEED, 0, out=z)
 elif name == "fused_f64":
     z = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
     fn = lambda: Q.qm_normal_philox(1 << 31, SEED, 0, dtype=torch.float64, out=z)
-elif name.startswith("config1_"):
+elif name.startswith("config1_") or name.startswith("plain_config1_"):
     import numpy as np
     from synth import inputs as I
     alg = {"breakless": Q.BREAKLESS, "as241": Q.AS241, "acklam": Q.ACKLAM, "refined": Q.ACKLAM_REFINED,
-           "moro": Q.MORO}[name[8:]]
+           "moro": Q.MORO}[name.split("config1_")[1]]
     u = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
     z = torch.empty_like(u)
-    fn = lambda: Q.qm_normal_quantile(u, out=z, alg=alg)
+    call = Q.qm_normal_quantile_plain if name.startswith("plain_") else Q.qm_normal_quantile
+    fn = lambda: call(u, out=z, alg=alg)
 elif name == "exp2n_f32":
     import numpy as np
     from synth import inputs as I
