@@ -139,11 +139,13 @@ qm_status qm_normal_philox(void *z, int64_t n, qm_precision p, qm_algorithm alg,
  *     nu = 10, K = 16, zstar = 6.9584  (4.1e-6)
  * (the last three: min-max crossovers of DESIGN.md reading R13, the paper gives
  * only nu = 4).  zstar <= 0 with any other (nu, K) -> QM_EUNSUPPORTED.  A caller
- * zstar > 0 is accepted for 1 <= nu <= 20, 1 <= K <= 24: the kernel then
+ * zstar > 0 is accepted for 2 <= nu <= 20, 1 <= K <= 24: the kernel then
  * evaluates the same composite with the caller's crossover and its error is the
  * caller's choice (tools/student_crossover.py computes min-max crossovers; the
- * tests cover nu in {1.5, 2, 7, 20} x K in {10, 16, 24} that way).  nu outside
- * [1, 20] -> QM_EUNSUPPORTED (the coefficient recurrence is ill-conditioned);
+ * tests cover nu in {2, 2.5, 7, 20} x K in {10, 16, 24} that way).  nu outside
+ * [2, 20] -> QM_EUNSUPPORTED (beyond 20 the coefficient recurrence is
+ * ill-conditioned; below 2 the tail's w^(-1/nu) amplifies the double erfcx's
+ * few-ulp error past the 2-ulp contract);
  * nu <= 0, K outside [1, 24] or a NaN zstar -> QM_EINVAL.
  * +-inf -> +-inf, NaN -> NaN; tail values beyond the double range -> +-inf. */
 qm_status qm_recycle_normal_to_t(const void *z, void *t, int64_t n, qm_precision p,

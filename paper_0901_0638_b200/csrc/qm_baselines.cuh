@@ -171,7 +171,7 @@ QM_DEV double breakless_plain(double u)
     const double z = -log(2.0 * vv);
     const double r = (ALG == ALG_BREAKLESS77) ? z * horner_plain<8>(kA77P_d, z) / horner_plain<8>(kA77Q_d, z)
                                               : z * horner_plain<14>(kD13P, z) / horner_plain<14>(kD13Q, z);
-    return specials_or(u, (u < 0.5) ? -r : r);
+    return specials_or(u, (u < 0.5) ? -fabs(r) : fabs(r));   // sgn = +1 at u = 1/2 (z = -0 there)
 }
 
 QM_DEV double as241_plain(double u)

@@ -190,7 +190,10 @@ qm_status student_setup(double nu, int K, double zstar, StudentParams *sp)
             if (d.nu == nu && d.K == K) zstar = d.zstar;
         if (zstar == 0.0) return QM_EUNSUPPORTED;   // no validated crossover for (nu, K)
     }
-    if (nu < 1.0 || nu > 20.0) return QM_EUNSUPPORTED;
+    // nu in [2, 20]: the recurrence is ill-conditioned beyond 20 (R22); below 2 the
+    // tail's w^(-1/nu) amplifies the double erfcx's few-ulp error by 1/nu past the
+    // 2-ulp contract (measured 2.19 ulp at nu = 1.5, 1.79 at nu = 2)
+    if (nu < 2.0 || nu > 20.0) return QM_EUNSUPPORTED;
     return student_params(nu, K, zstar, sp) ? QM_OK : QM_EUNSUPPORTED;
 }
 

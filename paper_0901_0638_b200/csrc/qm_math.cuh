@@ -442,6 +442,10 @@ enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5, ALG_F1212
 #ifndef QM_D13_KC
 #define QM_D13_KC 10     // compensated Horner steps of App D's 13 (A/B builds may override)
 #endif
+#ifndef QM_D13_KC_LO
+#define QM_D13_KC_LO 8   // ... for z <= QM_D13_ZSPLIT (written bound in rat64)
+#endif
+#define QM_D13_ZSPLIT 12.0
 
 template <int ALG> __host__ __device__ constexpr int fast_alg()
 {
@@ -485,10 +489,33 @@ QM_DEV double rat64(dd z)
     if (ALG == ALG_F1212) return rational_dd<13, 12>(z, kF12P, kF12Q);
     if (ALG == ALG_F88) return rational_dd<9, 8>(z, kF88P_d, kF88Q_d);
     if (ALG == ALG_BREAKLESS_TAIL)
-        return (z.hi < QM_VC_F64) ? rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q) : tail_model_q_dd(z);
-    // compensating the last 10 of 13 Horner steps is enough: 0.65 ulp max over
-    // 2^21 grid + tail-stratified inputs in emulation (all 13: 0.53; 9: 1.20)
-    return rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+        return (z.hi < QM_VC_F64) ? rat64<ALG_BREAKLESS>(z) : tail_model_q_dd(z);
+    // App D: compensate the last KC of the 13 Horner steps, KC from a written bound.
+    // The plain steps k >= KC add at most u (W_P(z) + W_Q(z)) relative error,
+    // W(z) = sum_{k >= KC} (sum_{i >= k} a_i z^i) / P(z) (all coefficients positive);
+    // with the double-double log and quotient and the final rounding the result is
+    // within W_P + W_Q + 0.5 + O(u) ulp.  max W_P + W_Q: KC = 10: 0.567 on z <= 36.04
+    // (the fp64 grid), 1.55 on z <= 74; KC = 8: 0.891 on z <= 12; KC = 9: 1.65 on
+    // z <= 36 (B200 measured 2.13 ulp: the bound is tight).  So z <= 12 takes KC = 8
+    // (two compensated steps = 16 FP64 operations fewer per sample), z > 12 KC = 10.
+    return (z.hi <= QM_D13_ZSPLIT) ? rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q)
+                                    : rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+}
+
+// The same value in warp-uniform code: every lane evaluates the cheap scheme; if
+// any lane of the warp has z > QM_D13_ZSPLIT (P = 1 - (1 - e^-12)^64 ~ 4e-4 per
+// 64-sample warp group) the warp also evaluates the other and each lane keeps its
+// own -- bitwise equal to rat64, with no divergent branch.
+template <int ALG>
+QM_DEV double rat64_warp(dd z)
+{
+    if (fast_alg<ALG>() != ALG_BREAKLESS) return rat64<fast_alg<ALG>()>(z);
+    double r = rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q);
+    if (__any_sync(0xffffffffu, !(z.hi <= QM_D13_ZSPLIT))) {
+        const double r2 = rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+        r = (z.hi <= QM_D13_ZSPLIT) ? r : r2;
+    }
+    return r;
 }
 
 // fast path: requires vv = min(u, 1-u) >= 2^-126 (normal, not NaN)
@@ -514,12 +541,13 @@ QM_DEV float nq_f32_careful(float u)
     return (vv >= 0.0f) ? r : __int_as_float(0x7fffffff);   // NaN, u < 0, u > 1
 }
 
+// warp-uniform callers only (rat64_warp votes)
 template <int ALG>
 QM_DEV double nq_f64_fast(double u)
 {
     const double omu = __dadd_rn(1.0, -u);
     const double vv = fmin(u, omu);
-    return apply_sign_f64(rat64<fast_alg<ALG>()>(neg_log2x_dd(vv, 0)), u, omu);
+    return apply_sign_f64(rat64_warp<ALG>(neg_log2x_dd(vv, 0)), u, omu);
 }
 
 template <int ALG>

@@ -13,7 +13,7 @@
 // with Q(0) = 0, Q'(0+-) = f0(0+-)/f(0).  Integrated forward from v = 0 this ODE
 // is exponentially ill-conditioned: Q' = 1 is a repelling fixed point
 // (d(Q'-1)/dv ~ (a-b)(Q'-1)), so an error e in Q'(0) grows like e^{(a-b)v}
-// (reading R26).  We therefore integrate BACKWARD, in the stable direction,
+// (reading R30).  We therefore integrate BACKWARD, in the stable direction,
 // from an anchor at |v| = Vmax (base probability e^-800) where Q is fixed by its
 // definition Fbar(Q(Vmax)) = p+ e^{-(a-b)Vmax} (tail mass by Gauss-Legendre
 // quadrature, Newton), down to v = 0 with classical RK4 in long double,

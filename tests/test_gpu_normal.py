@@ -190,22 +190,40 @@ def test_refined_acklam():
 
 
 # ------------------------- config 1 like-for-like: plain double
-@pytest.mark.parametrize("alg,name,nterms", [(Q.BREAKLESS, "d13", 14), (Q.BREAKLESS77, "a77", 8), (Q.AS241, "as241", 8),
-                                             (Q.ACKLAM, "acklam", 6), (Q.MORO, "moro", 9)])
+@pytest.mark.parametrize("alg,name,nterms", [(Q.BREAKLESS, "d13", 14), (Q.BREAKLESS77, "a77", 8), (Q.AS241, "as241", 8)])
 def test_plain_double_versions(alg, name, nterms):
     """qm_normal_quantile_plain: the same formulas coded in plain double like the
-    paper's Table 3 programs.  Bar: the plain-evaluation bound (2 N + 5) ulp of the
-    same formula (N = terms of the longer polynomial; 2N roundings of two Horner
-    chains, + log/sqrt, division and the final product); tail-stratified inputs
-    exercise every region."""
+    paper's Table 3 programs.  For these positive-coefficient rationals the plain
+    evaluation error is bounded by (2 N + 5) ulp of the same formula (N = terms of
+    the longer polynomial; 2N roundings of two Horner chains, + log/sqrt, division
+    and the final product); tail-stratified inputs exercise every region."""
     u = np.concatenate([I.tail_stratified((1 << 18) + 11, dtype=np.float64), I.mixed_uniforms(1 << 16, dtype=np.float64)])
     g = _gpu(Q.qm_normal_quantile_plain, u, alg=alg)
     ref = {"d13": lambda: O.normal_breakless(u, O.D13, 64), "a77": lambda: O.normal_breakless(u, O.A77, 64),
-           "as241": lambda: O.normal_as241(u, 64), "acklam": lambda: O.normal_acklam(u, 64, False),
-           "moro": lambda: O.normal_moro(u, 64)}[name]()
+           "as241": lambda: O.normal_as241(u, 64)}[name]()
     err = ulp_errors(g, ref, np.float64)
     print(name, "plain max ulp", summary(err))
     assert err.max() <= 2 * nterms + 5, summary(err)
+
+
+@pytest.mark.parametrize("alg,name,bound", [(Q.ACKLAM, "acklam", 1.15e-9), (Q.MORO, "moro", 3.1e-9)])
+def test_plain_double_mixed_sign_formulas(alg, name, bound):
+    """Acklam's and Moro's central rationals have coefficients of both signs, so
+    plain double loses digits to cancellation (no ulp bound of the formula); the
+    check is the formula's own accuracy against the exact quantile -- Acklam L1
+    1.15e-9 relative, Moro 3e-9 absolute for |x| <= 7 (R26) -- plus
+    2 ulp."""
+    u = np.concatenate([I.tail_stratified((1 << 18) + 11, dtype=np.float64), I.mixed_uniforms(1 << 16, dtype=np.float64)])
+    g = _gpu(Q.qm_normal_quantile_plain, u, alg=alg)
+    ex = O.ndtri_exact(u).astype(np.float64)
+    fin = np.isfinite(ex) & (np.abs(ex) <= 7)
+    if name == "acklam":
+        ok = np.abs(g[fin] - ex[fin]) <= bound * np.abs(ex[fin]) + 2 * np.spacing(np.abs(ex[fin]))
+    else:
+        ok = np.abs(g[fin] - ex[fin]) <= bound + 2 * np.spacing(np.abs(ex[fin]))
+    assert np.all(ok)
+    spec = ~np.isfinite(ex)
+    assert np.array_equal(g[spec], ex[spec], equal_nan=True)
 
 
 def test_plain_refined_acklam():

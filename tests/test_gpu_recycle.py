@@ -89,15 +89,16 @@ def test_student_caller_crossover_parity_and_bound(nu, K, zstar, bound):
 
 def test_student_unvalidated_default_is_unsupported():
     z = torch.zeros(8, dtype=torch.float64, device="cuda")
-    with pytest.raises(Q.QMError) as e:
-        Q.qm_recycle_normal_to_t(z, 7.0, 16, 0.0)
-    assert e.value.status == 2
+    for nu, K, zs in [(7.0, 16, 0.0), (1.5, 16, 2.39), (1.0, 16, 1.8), (21.0, 16, 9.9)]:
+        with pytest.raises(Q.QMError) as e:
+            Q.qm_recycle_normal_to_t(z, nu, K, zs)
+        assert e.value.status == 2
 
 
 def test_student_tail_beyond_double_range():
     """Tail values larger than the double range saturate to +-inf (t = F^-1(Phi(z)):
-    nu = 1 at |z| >= 38, nu = 3 at |z| = 70, 100), both precisions."""
-    for nu, K, zs, zz in [(1.0, 16, 1.8, [38.0, -38.0, 40.0, 100.0]), (3.0, 16, 3.5667, [70.0, -70.0, 100.0, -1e6])]:
+    nu = 2 at |z| >= 38, nu = 3 at |z| = 70, 100), both precisions."""
+    for nu, K, zs, zz in [(2.0, 16, 2.8008, [38.0, -38.0, 40.0, 100.0]), (3.0, 16, 3.5667, [70.0, -70.0, 100.0, -1e6])]:
         z = np.array(zz)
         g = Q.qm_recycle_normal_to_t(torch.from_numpy(z).cuda(), nu, K, zs).cpu().numpy()
         assert np.all(np.isinf(g)) and np.array_equal(np.sign(g), np.sign(z)), g

@@ -38,13 +38,27 @@ def test_recycle_exp_to_target_vs_exact_map(kind, par):
     # far tail out to e^-740 (the smallest double uniform gives e^-744)
     far = [1e-12, -1e-9, 40 / rr, -40 / rl, 40 / rr * (1 + 1e-9), 60.0, -70.0, 300 / rr, -500 / rl, 740 / rr, -740 / rl]
     real_lambda = kind == O.VG and par[0] != int(par[0])           # slower oracle (quadrature of K_nu)
-    v = np.concatenate([_base_samples(kind, par, 120 if real_lambda else 400), [0.0, -0.0], far])
+    v = np.concatenate([_base_samples(kind, par, 120 if real_lambda else 400), [0.0, -0.0], far,
+                        [1e-7, -3e-6, 2e-4, -2e-4, 1.5e-3, 4e-3]])          # the first node intervals
     fn = Q.qm_recycle_exp_to_hyperbolic if kind == O.HYPERBOLIC else Q.qm_recycle_exp_to_vg
     g = fn(torch.from_numpy(v).cuda(), tab).cpu().numpy()
     ex = O.recycle_exp_to_target(kind, par, v).astype(np.float64)
     nz = v != 0
+    bar = np.full(v.shape, 1e-14)
+    if real_lambda and par[0] < 2.5:
+        # inside the first node interval (|v| < h0 of its side) the quintic Hermite cannot
+        # follow the density's |x|^(2 lambda - 1) term at the origin (R29): the term's
+        # relative size at the first node, (alpha Q1)^(2 lambda - 1) (1 + |log alpha Q1|),
+        # bounds the interpolation error there (times 0.1: the Hermite fraction)
+        th = tab.cpu().numpy()
+        nodes1 = [th[80 + 4], th[80 + 4 * (4096 + 16384 + 4096 + 1) + 4]]     # Q at node 1, both sides
+        for side, h0 in ((0, th[32 + 1]), (1, th[32 + 24 + 1])):
+            aq = par[1] * abs(nodes1[side])
+            b1 = max(1e-14, 0.1 * aq ** (2 * par[0] - 1) * (1 + abs(np.log(aq))))
+            sel = (np.abs(v) < h0) & ((v < 0) == (side == 1))
+            bar[sel] = b1
     rel = np.abs(g[nz] / ex[nz] - 1)
-    assert rel.max() < 1e-14, (rel.max(), v[nz][np.argmax(rel)])
+    assert np.all(rel <= bar[nz]), (np.max(rel / bar[nz]), v[nz][np.argmax(rel / bar[nz])])
     assert g[~nz].tolist() == v[~nz].tolist() and np.array_equal(np.signbit(g[~nz]), np.signbit(v[~nz]))
     g32 = fn(torch.from_numpy(v.astype(np.float32)).cuda(), tab).cpu().numpy()
     ex32 = O.recycle_exp_to_target(kind, par, v.astype(np.float32).astype(np.float64))

@@ -294,3 +294,25 @@ def test_moro_regions_and_symmetry():
     assert sp[0] == -np.inf and sp[1] == np.inf and sp[2] == 0 and not np.signbit(sp[2])
     assert np.all(np.isnan(sp[3:]))
 
+
+
+def test_d13_partial_compensation_bound():
+    """The written bound behind the product's App D scheme (qm_math.cuh rat64): the
+    Horner steps left uncompensated add at most u (W_P(z) + W_Q(z)) relative error,
+    W(z) = sum over plain steps k of sum_{i>=k} a_i z^i / P(z) (all App D coefficients
+    are positive).  Compensating 8 steps for z <= 12 and 10 beyond keeps
+    W_P + W_Q < 0.9 resp. < 0.6 on the fp64 grid (z <= 36.04): with the final rounding
+    the result stays inside the 2-ulp contract; 9 steps would not (1.65 + 0.5)."""
+    p, q = O.coeffs(O.D13, 64)
+    p, q = p.astype(np.float64), q.astype(np.float64)
+
+    def W(c, z, kc):
+        t = c * z ** np.arange(c.size)
+        return sum(t[k:].sum() / t.sum() for k in range(kc, c.size - 1))
+
+    def mx(kc, zmax):
+        return max(W(p, z, kc) + W(q, z, kc) for z in np.linspace(0.0, zmax, 4001))
+
+    assert mx(8, 12.0) < 0.9
+    assert mx(10, 36.04) < 0.6
+    assert mx(9, 36.04) > 1.5          # the bound is what rules 9 steps out (measured 2.13 ulp on B200)

@@ -27,7 +27,10 @@ for name, n in ELEMS.items():
     out[name] = {"kernel": k["kernel"],
                  "dram_bytes_per_elem": (k.get("dram_read_bytes", 0) + k.get("dram_write_bytes", 0)) / n,
                  "warp_inst_per_elem": k.get("warp_inst_executed", 0) / n,
-                 "fp64_inst_per_elem": k.get("fp64_inst_executed", 0) / n,
+                 # FP64-pipe warp-instructions per sample: the pipe's % of its peak
+                 # (0.5 warp-inst/cycle/SMSP, 592 SMSPs) x the launch's cycles (ncu duration x clock)
+                 "fp64_inst_per_elem": (k.get("fp64_pipe_pct", 0) / 100 * 592 * 0.5 *
+                                        k.get("duration_us", 0) * 1e-6 * k.get("sm_clock_hz", 0) / n),
                  "source": f"{p} (ncu --set full, one launch of {n} samples)"}
     for key in ("fp64_pipe_pct", "fma_pipe_pct", "alu_pipe_pct", "xu_pipe_pct", "issue_active_pct",
                 "divergent_branch_targets", "threads_per_inst", "registers"):

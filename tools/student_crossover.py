@@ -29,7 +29,7 @@ def minmax_crossover(n, K):
 
 
 # caller-supplied crossovers tested beside the shipped table (qm.h): nu x K grid
-CALLER_GRID = [(n, K) for n in (1.5, 2.0, 7.0, 20.0) for K in (10, 16, 24)]
+CALLER_GRID = [(n, K) for n in (2.0, 2.5, 7.0, 20.0) for K in (10, 16, 24)]
 
 if __name__ == "__main__":
     for n, K in [(3.0, 16), (5.0, 16), (10.0, 16)]:
