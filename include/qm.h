@@ -229,13 +229,15 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
  *    (half-integer Bessel orders in closed form) or real 1.1 <= lambda <= 30
  *    (K of real order by Temme's series / Steed's continued fraction; the
  *    origin, where the density is not analytic for non-integer lambda, is
- *    approached on a geometric mesh -- the "many steps near v = 0" of P:395).
+ *    approached on geometric meshes and the centre nodes are graded towards it,
+ *    w_k = Wc (k/4096)^4 -- the "many steps near v = 0" of P:395).
  *    Bad parameters -> QM_EINVAL; lambda < 1 (out of scope),
  *    1 < lambda < 1.1 or lambda > 30 -> QM_EUNSUPPORTED.
  *  - qm_recycle_exp_to_hyperbolic / qm_recycle_exp_to_vg: x[i] = Q(v[i]) for
  *    base samples v (quintic Hermite on (Q, Q', Q'') at 24577 nodes per side:
- *    4096 on the centre rate*|v| <= 2, 16384 out to base probability e^-40,
- *    4096 out to e^-800; linear beyond).  +-0, +-inf, NaN pass through.
+ *    4096 on the centre rate*|v| <= 2 (uniform, or graded as above), 16384 out
+ *    to base probability e^-40, 4096 out to e^-800; linear beyond).  +-0, +-inf,
+ *    NaN pass through.
  *  - qm_exp_base_quantile: v[i] = Q0(u[i]) of P:322-329.
  *  - qm_exp_target_philox: fused Philox (qm_philox_uniform layout) -> Q0 -> Q.
  * Accuracy (the method's, against the exact map): < 2e-12 relative in fp64

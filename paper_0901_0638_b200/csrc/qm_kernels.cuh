@@ -214,6 +214,7 @@ struct TlCfg {
 using TlCfgJ = TlCfg<16, 4, 8192, 1>;       // 1 CTA/SM, 16 consumer warps, 4 x 32 KB
 using TlCfgK = TlCfg<16, 3, 8192, 2>;       // 2 CTAs/SM, 2 x 3 x 32 KB
 using TlCfgL = TlCfg<16, 4, 8192, 1, 2>;    // J, 2 float4 per vote
+using TlCfgM = TlCfg<8, 3, 8192, 2, 2>;     // 2 CTAs/SM of 8 consumer warps, 2 x 3 x 32 KB
 
 template <int ALG, class CFG>
 __global__ void __launch_bounds__(CFG::THREADS, CFG::MINB)

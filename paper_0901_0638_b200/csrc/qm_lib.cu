@@ -116,12 +116,12 @@ qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64
     return launched();
 }
 
-// QM_TL_CFG=J|K|L selects the TMA-in/STG-out shape (default L)
+// QM_TL_CFG=J|K|L|M selects the TMA-in/STG-out shape (default L)
 char tl_cfg()
 {
     static const char c = [] {
         const char *e = getenv("QM_TL_CFG");
-        return (e && e[0] >= 'J' && e[0] <= 'L') ? e[0] : 'L';
+        return (e && e[0] >= 'J' && e[0] <= 'M') ? e[0] : 'L';
     }();
     return c;
 }
@@ -135,6 +135,7 @@ qm_status normal_f32(const float *u, float *z, int64_t n, cudaStream_t s)
         switch (tl_cfg()) {
         case 'K': return launch_stream_f32<TlCfgK>(k_normal_f32_tl<ALG, TlCfgK>, k_normal_f32<ALG>, u, z, n, s);
         case 'L': return launch_stream_f32<TlCfgL>(k_normal_f32_tl<ALG, TlCfgL>, k_normal_f32<ALG>, u, z, n, s);
+        case 'M': return launch_stream_f32<TlCfgM>(k_normal_f32_tl<ALG, TlCfgM>, k_normal_f32<ALG>, u, z, n, s);
         default: return launch_stream_f32<TlCfgJ>(k_normal_f32_tl<ALG, TlCfgJ>, k_normal_f32<ALG>, u, z, n, s);
         }
     }

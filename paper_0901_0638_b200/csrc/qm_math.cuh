@@ -197,10 +197,27 @@ QM_DEV float2 neg_log2x_f32x2(float vva, float vvb, int eadj = 0)
 
 // |z P(z)/Q(z)| for the fp32 formulas: coefficients float-rounded, evaluated in
 // FP64 (N coefficients each), rcp seed + one quotient correction, one rounding.
+#ifndef QM_F32_XU_LITE
+#define QM_F32_XU_LITE 0   // A/B: 1 = float<->double conversions by integer ops (XU relief)
+#endif
+// float -> double by bits for z >= +-0 finite (sign cleared: -0 -> +2^-127, which the
+// final multiply by the float z turns back into 0)
+QM_DEV double widen_pos(float z)
+{
+    const uint32_t f = __float_as_uint(z) & 0x7fffffffu;
+    return __hiloint2double((int)((f >> 3) + 0x38000000u), (int)(f << 29));
+}
+// double in [2^-126, 2^127) -> float by truncation (funnel shift + exponent rebias)
+QM_DEV float narrow_trunc(double t)
+{
+    const uint32_t fb = __funnelshift_l((uint32_t)__double2loint(t), (uint32_t)__double2hiint(t), 3) - 0xC0000000u;
+    return __uint_as_float(fb);
+}
+
 template <int N, bool CORRECT = true>
 QM_DEV float rational_f32path(float z, const double *P, const double *Q)
 {
-    const double zd = (double)z;
+    const double zd = QM_F32_XU_LITE ? widen_pos(z) : (double)z;
     double p = P[N - 1], q = Q[N - 1];
 #pragma unroll
     for (int i = N - 2; i >= 0; --i) {
@@ -220,7 +237,7 @@ QM_DEV float rational_f32path(float z, const double *P, const double *Q)
     // z (P/Q) with P/Q rounded to float and the product in fp32: one DMUL fewer
     // on the FP64 pipe (the kernel's co-bottleneck) for +0.5 ulp: <= 2.41 ulp over
     // the fp32 grid in emulation (final DMUL: 1.67)
-    return __fmul_rn(__double2float_rn(t), z);
+    return __fmul_rn(QM_F32_XU_LITE ? narrow_trunc(t) : __double2float_rn(t), z);
 #endif
 }
 
@@ -446,6 +463,9 @@ enum { ALG_BREAKLESS = 0, ALG_BREAKLESS77 = 1, ALG_BREAKLESS_TAIL = 5, ALG_F1212
 #define QM_D13_KC_LO 8   // ... for z <= QM_D13_ZSPLIT (written bound in rat64)
 #endif
 #define QM_D13_ZSPLIT 12.0
+#ifndef QM_D13_SPLIT
+#define QM_D13_SPLIT 0    // A/B: 1 = the z <= 12 / z > 12 split of rat64 (measured slower, see there)
+#endif
 
 template <int ALG> __host__ __device__ constexpr int fast_alg()
 {
@@ -498,8 +518,14 @@ QM_DEV double rat64(dd z)
     // (the fp64 grid), 1.55 on z <= 74; KC = 8: 0.891 on z <= 12; KC = 9: 1.65 on
     // z <= 36 (B200 measured 2.13 ulp: the bound is tight).  So z <= 12 takes KC = 8
     // (two compensated steps = 16 FP64 operations fewer per sample), z > 12 KC = 10.
-    return (z.hi <= QM_D13_ZSPLIT) ? rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q)
-                                    : rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+    // That split (QM_D13_SPLIT=1) measured: fused fp64 +6.5 % (61.3 vs 57.6 Gsamples/s),
+    // but the TMA map -11 % (58 vs 65: the per-pair votes break the interleaving of
+    // the pairs' chains, 128 registers) and tail-stratified config 1 -34 % (most
+    // warps pay both schemes) -- so the product keeps KC = 10 for every z.
+    if (QM_D13_SPLIT)
+        return (z.hi <= QM_D13_ZSPLIT) ? rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q)
+                                        : rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+    return rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
 }
 
 // The same value in warp-uniform code: every lane evaluates the cheap scheme; if
@@ -509,7 +535,7 @@ QM_DEV double rat64(dd z)
 template <int ALG>
 QM_DEV double rat64_warp(dd z)
 {
-    if (fast_alg<ALG>() != ALG_BREAKLESS) return rat64<fast_alg<ALG>()>(z);
+    if (fast_alg<ALG>() != ALG_BREAKLESS || !QM_D13_SPLIT) return rat64<fast_alg<ALG>()>(z);
     double r = rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q);
     if (__any_sync(0xffffffffu, !(z.hi <= QM_D13_ZSPLIT))) {
         const double r2 = rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);

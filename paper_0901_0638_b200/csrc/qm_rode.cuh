@@ -57,7 +57,11 @@ QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
 struct RodePrep {
     const double *b;     // node k of the sample's side (shared or global memory)
     int st;              // doubles from node k to node k+1 (3 shared, 4 global)
-    double t, h, a, vmax;
+    double t, a, vmax;
+    // dw/ds and d2w/ds2 at nodes k and k+1 (s = the node coordinate): h and 0 on a
+    // uniform segment; on the graded centre segment of a real-lambda VG table
+    // (w = Wc (s/n)^4, qm_rode_host.cpp): 4 G s^3 and 12 G s^2, G = Wc/n^4
+    double ws0, ws1, wss0, wss1;
 };
 
 // per-side segment boundaries Wc, V and Vmax, held in registers (loaded once
@@ -80,10 +84,13 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     const double wc = side ? bd.wc1 : bd.wc0, vb = side ? bd.v1 : bd.v0;
     // segment j = [a >= Wc] + [a >= V] (selects; NaN lands in j = 0 and is replaced later)
     const int j = (a >= wc) + (a >= vb);
-    // the segment record (w0, h | 1/h, k0 | n, w1) as three 16-byte shared loads
+    // the segment record (w0, h | 1/h, k0 | n, w1 | G, graded) as four 16-byte shared loads
     const double2 *r = reinterpret_cast<const double2 *>(sm + QM_RODE_SEG + 24 * side + 8 * j);
-    const double2 r01 = r[0], r23 = r[1], r45 = r[2];
-    const double s = fmin((a - r01.x) * r23.x, r45.x);          // local coordinate in [0, n]
+    const double2 r01 = r[0], r23 = r[1], r45 = r[2], r67 = r[3];
+    double s = (a - r01.x) * r23.x;                             // local coordinate in [0, n]
+    const bool graded = r67.y != 0.0;                           // real-lambda VG centre (r23.x = 1/Wc)
+    if (graded) s = r45.x * sqrt(sqrt(a * r23.x));
+    s = fmin(s, r45.x);
     const double fk = fmin(floor(s), r45.x - 1.0);
     const int k = (int)r23.y + (int)fk;
     const bool in_sm = (M > 0) && (j == 0) && (k + 1 < M);
@@ -91,9 +98,13 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     p.b = in_sm ? sm + kRodeSmHdr + 3 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
     p.st = in_sm ? 3 : 4;
     p.t = s - fk;
-    p.h = r01.y;
     p.a = a;
     p.vmax = side ? bd.vm1 : bd.vm0;
+    const double k1 = fk + 1.0;
+    p.ws0 = graded ? 4.0 * r67.x * fk * fk * fk : r01.y;
+    p.ws1 = graded ? 4.0 * r67.x * k1 * k1 * k1 : r01.y;
+    p.wss0 = graded ? 12.0 * r67.x * fk * fk : 0.0;
+    p.wss1 = graded ? 12.0 * r67.x * k1 * k1 : 0.0;
     return p;
 }
 
@@ -114,9 +125,12 @@ QM_DEV RodeNodes rode_load(const RodePrep &p)
 // quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
 QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
 {
-    const double h = p.h, t = p.t;
-    const double m0 = h * n.d0, m1 = h * n.d1, h2 = h * h;
-    const double a0 = h2 * n.dd0, a1 = h2 * n.dd1, dp = n.r1 - n.r0;
+    const double t = p.t;
+    // derivatives with respect to s: dR/ds = R' w_s, d2R/ds2 = R'' w_s^2 + R' w_ss
+    const double m0 = p.ws0 * n.d0, m1 = p.ws1 * n.d1;
+    const double a0 = __fma_rn(p.ws0 * p.ws0, n.dd0, p.wss0 * n.d0);
+    const double a1 = __fma_rn(p.ws1 * p.ws1, n.dd1, p.wss1 * n.d1);
+    const double dp = n.r1 - n.r0;
     const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
     const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
     const double c5 = 6.0 * dp - 3.0 * m0 - 3.0 * m1 - 0.5 * a0 + 0.5 * a1;

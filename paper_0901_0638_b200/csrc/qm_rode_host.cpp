@@ -24,6 +24,7 @@
 // where Q -> 0).
 //
 // Table layout (doubles): see qm_rode.cuh.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <cstdint>
@@ -271,6 +272,13 @@ bool rode_table_build(int kind, const double *params, double *tab)
     const int Nc = QM_RODE_CENTRE_NODES, N = QM_RODE_NODES, M = QM_RODE_TAIL_NODES, NT = QM_RODE_NT;
     std::memset(tab, 0, QM_RODE_HEADER * sizeof(double));
 
+    // real-order VG: the density is A(x^2) + |x|^(2 nu) B(x^2) at the origin (R29), so
+    // the map has a v^(2 lambda) term there that a quintic Hermite on uniform nodes
+    // cannot follow.  Its centre segment is graded, node k at w_k = Wc (k/Nc)^4: in
+    // the node coordinate s the term becomes s^(8 lambda) (smooth to the 6th order),
+    // the regular w^2 term s^8 (the quintic's error on it is ~w_1 = 7e-15 Wc relative)
+    // and the far end is 4x coarser in w than a uniform segment.
+    const bool graded = (t.kind == QM_RODE_VG && t.m < 0);
     for (int side = 0; side < 2; ++side) {
         const ld rate = side == 0 ? rr : rl, p = side == 0 ? pp : pm;
         const int dir = side == 0 ? +1 : -1;
@@ -288,7 +296,17 @@ bool rode_table_build(int kind, const double *params, double *tab)
             rec[3] = k0[j];
             rec[4] = nseg[j];
             rec[5] = (double)w1[j];
+            if (j == 0 && graded) {               // kernel: s = n (w / Wc)^(1/4), w_s = 4 G s^3, G = Wc/n^4
+                rec[2] = (double)(1.0L / Wc);
+                rec[6] = (double)(Wc / ((ld)Nc * Nc * Nc * Nc));
+                rec[7] = 1.0;
+            }
         }
+        auto wnode = [&](int k) {                 // centre node positions
+            if (!graded) return (ld)k * hs[0];
+            const ld x = (ld)k / (ld)Nc;
+            return Wc * (x * x) * (x * x);
+        };
         auto seg_of = [&](int k) { return k >= k0[2] ? 2 : (k >= k0[1] ? 1 : 0); };   // interval [k, k+1]
 
         // anchor: tail mass of the target beyond Q(Vmax) equals the base's, p e^{-rate Vmax}
@@ -341,7 +359,6 @@ bool rode_table_build(int kind, const double *params, double *tab)
         // real-order VG: H has a |Q|^(2 nu - 1) (or Q log Q) term at the origin, so the
         // interval next to v = 0 is stepped on a geometric mesh (w_i = h0 r^-i): RK4's
         // error there scales with the local step over the distance to 0, not with h0
-        const bool graded = (t.kind == QM_RODE_VG && t.m < 0);
         constexpr int NG = 4800;                               // r = 1.005: h0 r^-4800 ~ 4e-11 h0 (r = 1.12 left 1e-13 at lambda = 1.5,
                                                                // 1.02 left 5e-15 at lambda = 1.2; 1.005 converged to 1e-17 at 1.1)
         const ld rg = 1.005L;
@@ -376,16 +393,29 @@ bool rode_table_build(int kind, const double *params, double *tab)
         cQ = cP = 0.0L;
         put(0, Q, P);
         for (int k = 1; k <= Nc; ++k) {
-            if (k == 1 && graded) {
+            if (graded) {
+                // geometric substeps (ratio <= rg) from node k-1 to node k; from 0 to node 1
+                // down to 4e-11 of it first
+                const ld wa = wnode(k - 1), wb = wnode(k);
                 ld w = 0.0L;
-                for (int i = NG; i >= 0; --i) {
-                    const ld wn = hs[0] * powl(rg, -(ld)i);
-                    rk4(Q, P, wn - w);
-                    w = wn;
+                if (k == 1) {
+                    for (int i = NG; i >= 1; --i) {
+                        const ld wn = wb * powl(rg, -(ld)i);
+                        rk4(Q, P, wn - w);
+                        w = wn;
+                    }
+                    rk4(Q, P, wb - w);
+                } else {
+                    const int ns = std::max(4 * sub, (int)ceill(logl(wb / wa) / logl(rg)));
+                    w = wa;
+                    for (int i = 1; i <= ns; ++i) {
+                        const ld wn = (i == ns) ? wb : wa * powl(wb / wa, (ld)i / (ld)ns);
+                        rk4(Q, P, wn - w);
+                        w = wn;
+                    }
                 }
             } else {
-                const int ns = (graded && k <= 64) ? sub * (64 / k) : sub;    // interval [k-1, k]: finer near 0
-                for (int j = 0; j < ns; ++j) rk4(Q, P, hs[0] / ns);
+                for (int j = 0; j < sub; ++j) rk4(Q, P, hs[0] / sub);
             }
             if (k < Nc) put(k, Q, P);
         }

@@ -14,7 +14,10 @@
 // table[12+s] Q(0) residual of the backward sweep           table[14+s] its slope residual
 // table[16+s], table[18+s]: log p_s as hi + lo              table[20+s] 1/rate_s
 // table[22+s] forward/backward mismatch of Q at w = Wc      table[28+s] Vmax_s    table[30] 3
-// segment record (s, j) at table[32 + 8 (3 s + j)]: w0, h, 1/h, k0, n (intervals), w1, 0, 0
+// segment record (s, j) at table[32 + 8 (3 s + j)]: w0, h, 1/h, k0, n (intervals), w1, G, graded
+//   graded = 1 only for the centre segment (j = 0) of a real-lambda VG table: its nodes
+//   sit at w_k = Wc (k/n)^4 (G = Wc/n^4, and the 1/h slot holds 1/Wc), so that the
+//   map's non-analytic v^(2 lambda) term at the origin is resolved (R29)
 // nodes of side s at table[QM_RODE_HEADER + s*4*(QM_RODE_NT+1)]: (R_k, R'_k, R''_k, 0),
 // k = 0..NT, R' = dR/dw (negative on the left side), R'' from the RODE itself
 // (R'' = H(R) R'^2 - rate R'); quintic Hermite interpolation.

@@ -97,8 +97,9 @@ def test_student_unvalidated_default_is_unsupported():
 
 def test_student_tail_beyond_double_range():
     """Tail values larger than the double range saturate to +-inf (t = F^-1(Phi(z)):
-    nu = 2 at |z| >= 38, nu = 3 at |z| = 70, 100), both precisions."""
-    for nu, K, zs, zz in [(2.0, 16, 2.8008, [38.0, -38.0, 40.0, 100.0]), (3.0, 16, 3.5667, [70.0, -70.0, 100.0, -1e6])]:
+    nu = 2 from |z| ~ 52.7, nu = 3 from ~ 43), both precisions; below, finite values
+    within the bar."""
+    for nu, K, zs, zz in [(2.0, 16, 2.8008, [60.0, -60.0, 100.0, 1e6]), (3.0, 16, 3.5667, [70.0, -70.0, 100.0, -1e6])]:
         z = np.array(zz)
         g = Q.qm_recycle_normal_to_t(torch.from_numpy(z).cuda(), nu, K, zs).cpu().numpy()
         assert np.all(np.isinf(g)) and np.array_equal(np.sign(g), np.sign(z)), g
@@ -106,6 +107,9 @@ def test_student_tail_beyond_double_range():
         assert ulp_errors(g, ref, np.float64).max() == 0.0
         g32 = Q.qm_recycle_normal_to_t(torch.from_numpy(z.astype(np.float32)).cuda(), nu, K, zs).cpu().numpy()
         assert np.all(np.isinf(g32)) and np.array_equal(np.sign(g32), np.sign(z)), g32
+    z = np.array([38.0, -38.0, 45.0, 52.0])                   # nu = 2: large but finite
+    g = Q.qm_recycle_normal_to_t(torch.from_numpy(z).cuda(), 2.0, 16, 2.8008).cpu().numpy()
+    assert np.all(np.isfinite(g)) and ulp_errors(g, O.student_map(z, 2.0, 16, 2.8008), np.float64).max() <= 2.0
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])

@@ -124,16 +124,20 @@ def test_product_rode_table_vs_oracle(kind, par):
         nodes = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)
         assert nodes[0, 0] == 0.0
         for j, js in enumerate([[1, 2, 37, 4000], [1, 500, 5000, 16383], [1, 100, 2000, 4096]]):
-            w0, h, ih, k0, n, w1 = tab[SEG + 8 * (3 * side + j):SEG + 8 * (3 * side + j) + 6]
+            w0, h, ih, k0, n, w1, G, graded = tab[SEG + 8 * (3 * side + j):SEG + 8 * (3 * side + j) + 8]
             assert int(k0) == [0, 4096, 4096 + 16384][j] and abs(w0 + n * h - w1) <= 1e-12 * w1
             js = np.array(js)
-            ex = O.recycle_exp_to_target(kind, par, (w0 + js * h) * sg).astype(np.float64)
+            # real-lambda VG: centre nodes at Wc (k/n)^4 (graded, R29)
+            wk = G * js.astype(np.float64) ** 4 if graded else w0 + js * h
+            assert (graded == 0) or (j == 0 and kind == O.VG and par[0] != int(par[0]))
+            ex = O.recycle_exp_to_target(kind, par, wk * sg).astype(np.float64)
             assert np.abs(nodes[int(k0) + js, 0] / ex - 1).max() < 1e-13, j
         # R' and R'' against central differences of the exact map (long double; O(hh^2) ~ 1e-8)
-        w0, h = tab[SEG + 8 * 3 * side], tab[SEG + 8 * 3 * side + 1]
-        ks = np.array([1, 2, 37, 500])
+        w0, h, G, graded = tab[SEG + 8 * 3 * side], tab[SEG + 8 * 3 * side + 1], tab[SEG + 8 * 3 * side + 6], \
+            tab[SEG + 8 * 3 * side + 7]
+        ks = np.array([1, 2, 37, 500]) if not graded else np.array([300, 500, 1000, 2000])
+        w = G * ks.astype(np.float64) ** 4 if graded else ks * h
         hh = 1e-2 * h
-        w = ks * h
         qp = O.recycle_exp_to_target(kind, par, (w + hh) * sg)
         q0 = O.recycle_exp_to_target(kind, par, w * sg)
         qm = O.recycle_exp_to_target(kind, par, (w - hh) * sg)

@@ -17,6 +17,17 @@ prof() {  # name regex [env] [prof_kernel name]
       -o /tmp/prof_$1 -f python tools/prof_kernel.py ${4:-$1} 3 > $OUT/profiles/ncu_$1.log 2>&1
   python tools/ncu_summary.py /tmp/prof_$1.ncu-rep > $OUT/profiles/ncu_$1.json 2>>$OUT/profiles/ncu_$1.log
 }
+want() { [ "${PROFS:-all}" = all ] || [[ " ${PROFS} " == *" $1 "* ]]; }
+if [ "${PROFS:-all}" != all ] && [ "${PROFS}" != none ]; then
+  want stream_f32 && { prof stream_f32 k_normal_f32_tl; cp /tmp/prof_stream_f32.ncu-rep $OUT/; }
+  want stream_f64 && prof stream_f64 k_normal_f64_tl
+  want fused_f64 && prof fused_f64 k_philox_f64
+  want student && prof student k_student_f64_tl
+  want student_moments && prof student_moments k_student_moments_tl
+  want config1_breakless && prof config1_breakless "k_normal_f64" "" config1_breakless
+  want fused_f32 && prof fused_f32 k_philox_f32
+  want rode_hyp_f64 && prof rode_hyp_f64 k_rode_map_tl
+fi
 if [ "${PROFS:-all}" = all ]; then
   prof stream_f32 k_normal_f32_tl; cp /tmp/prof_stream_f32.ncu-rep $OUT/
   prof stream_f64 k_normal_f64_tl
