@@ -84,6 +84,7 @@ def lib():
             "orc_student_branches": (i32, [P, P, P, i64, dbl, i32, P]),
             "orc_student_exact": (i32, [P, P, i64, dbl]),
             "orc_student_cdf_upper_v": (None, [P, P, i64, dbl]),
+            "orc_student_rode": (i32, [P, P, i64, dbl, dbl]),
             "orc_moments_f64": (None, [P, i64, i32, P]),
             "orc_moments_f32": (None, [P, i64, i32, P]),
             "orc_mc_call": (None, [i64, u64, u64, dbl, dbl, dbl, dbl, P, i32, P]),
@@ -353,6 +354,13 @@ def student_branches(z, n: float, K: int):
 def student_exact(z, n: float) -> np.ndarray:
     z = _in(z); o = np.empty(z.shape, np.longdouble)
     _chk(lib().orc_student_exact(_p(z), _p(o), z.size, n))
+    return o
+
+
+def student_rode(z, n: float, h: float = 1e-3) -> np.ndarray:
+    """Student map by the forward RK4 solution of the Recycling ODE."""
+    z = _in(z); o = np.empty(z.shape, np.longdouble)
+    _chk(lib().orc_student_rode(_p(z), _p(o), z.size, n, h))
     return o
 
 
