@@ -361,6 +361,13 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     for nu, K in [(4.0, 10), (3.0, 16), (5.0, 16), (10.0, 16)]:
         rec(f"student_f64_nu{int(nu)}_K{K}_2^30", lambda nu=nu, K=K: Q.qm_recycle_normal_to_t(zn, nu, K, out=tt),
             1 << 30, 16, "hbm", "student" if nu == 4.0 else None)
+    # §3.6's purely numerical method: the same config-4 samples through the
+    # RODE table (any nu, no crossover; < 2e-14 against the exact map)
+    for nu in (3.0, 5.0, 10.0):
+        tab_s = Q.qm_normal_target_table(Q.STUDENT, [nu])
+        rec(f"student_rode_f64_nu{int(nu)}_2^30", lambda tab_s=tab_s: Q.qm_recycle_normal_to_t_rode(zn, tab_s, out=tt),
+            1 << 30, 16, "hbm", "student_rode" if nu == 5.0 else None)
+    del tab_s
     rows4 = torch.empty((Q.qm_moment_row_count(1 << 30), 4), dtype=torch.float64, device="cuda")
     rec("student_moments_f64_nu5_K16_2^30",
         lambda: Q.qm_recycle_normal_to_t_moments(zn, 5.0, 16, out=tt, rows=rows4), 1 << 30, 16, "hbm",

@@ -243,7 +243,7 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
  * Accuracy (the method's, against the exact map): < 2e-12 relative in fp64
  * (worst near v = 0), correctly rounded to within 2 ulp in fp32. */
 #define QM_RODE_TABLE_DOUBLES (80 + 8 * (4096 + 16384 + 4096 + 1))
-typedef enum { QM_TARGET_HYPERBOLIC = 1, QM_TARGET_VG = 2 } qm_target;
+typedef enum { QM_TARGET_HYPERBOLIC = 1, QM_TARGET_VG = 2, QM_TARGET_STUDENT = 3 } qm_target;
 qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev);
 qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p,
                                        const double *table_dev, void *stream);
@@ -253,6 +253,31 @@ qm_status qm_exp_base_quantile(const void *u, void *v, int64_t n, qm_precision p
                                const double *table_dev, void *stream);
 qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double *table_dev,
                                uint64_t seed, uint64_t counter_offset, void *stream);
+/* Gaussian-base recycling by the "purely numerical method" of §3.6:
+ * the Student Recycling ODE solved numerically and sampled by
+ * interpolation -- the alternative to the series of qm_recycle_normal_to_t,
+ * with no crossover and no restriction to a validated (nu, K).
+ *  - qm_normal_target_table(QM_TARGET_STUDENT, {nu}, table_dev) builds the map
+ *    t = F_nu^-1(Phi(z)) into a caller-owned DEVICE buffer of
+ *    QM_RODE_TABLE_DOUBLES doubles (the layout of the exponential-base tables):
+ *    host setup (~0.2 s) integrating the RODE in long double BACKWARD from an
+ *    anchor at |z| = 38.5 (beyond the largest |z| a double uniform can give),
+ *    where t is fixed by its definition -- forward from the centre conditions
+ *    Q(0) = 0, Q'(0) = gamma the error grows like e^{z^2/2} --, in
+ *    log t beyond |z| = 2; the centre |z| <= 2 is redone forward from the exact
+ *    centre conditions.  1 <= nu <= 200; nu <= 0 or a wrong kind -> QM_EINVAL,
+ *    0 < nu < 1 or nu > 200 -> QM_EUNSUPPORTED.  Synchronous.
+ *  - qm_recycle_normal_to_t_rode: t[i] = A(z[i]) for normal samples z (fp32 or
+ *    fp64, any alignment, caller's stream): quintic Hermite on (Q, Q', Q'') at
+ *    4097 nodes on |z| <= 2, 16384 on 2..6, and on (log|Q|)', (log|Q|)'' at 4096
+ *    on 6..38.5 (exponentiated; log-linear beyond).  +-0, +-inf, NaN pass
+ *    through; values beyond the double range -> +-inf.
+ * Accuracy against the exact map: < 2e-14 relative on |z| <= 6 (the paper's
+ * claim there is 5e-8), and within 2e-14 + 8 eps |log t| beyond (the
+ * interpolated quantity is log t). */
+qm_status qm_normal_target_table(qm_target kind, const double *params, double *table_dev);
+qm_status qm_recycle_normal_to_t_rode(const void *z, void *t, int64_t n, qm_precision p,
+                                      const double *table_dev, void *stream);
 /* the same table in HOST memory (diagnostics: header + nodes, see qm_rode_params.h) */
 int qm_rode_table_host(int kind, const double *params, double *table);
 

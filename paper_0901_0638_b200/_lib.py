@@ -19,7 +19,7 @@ QM_BREAKLESS, QM_BREAKLESS77, QM_AS241, QM_ACKLAM, QM_ACKLAM_REFINED, QM_BREAKLE
 QM_BREAKLESS1212, QM_BREAKLESS88, QM_TWO_REGION = 7, 8, 9
 QM_MOMENT_CHUNK = 65536
 QM_MC_CHUNK = 1 << 20
-QM_TARGET_HYPERBOLIC, QM_TARGET_VG = 1, 2
+QM_TARGET_HYPERBOLIC, QM_TARGET_VG, QM_TARGET_STUDENT = 1, 2, 3
 QM_RODE_TABLE_DOUBLES = 80 + 8 * (4096 + 16384 + 4096 + 1)
 QM_MC_MAX_STRIKES = 32
 
@@ -45,6 +45,8 @@ SIGNATURES = {
     "qm_recycle_normal_to_t_moments": (_I32, [_P, _P, _I64, _I32, _D, _I32, _D, _P, _P]),
     "qm_recycle_exp_to_normal": (_I32, [_P, _P, _I64, _I32, _I32, _P]),
     "qm_exp_target_table": (_I32, [_I32, _P, _P]),
+    "qm_normal_target_table": (_I32, [_I32, _P, _P]),
+    "qm_recycle_normal_to_t_rode": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "qm_recycle_exp_to_hyperbolic": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "qm_recycle_exp_to_vg": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "qm_exp_base_quantile": (_I32, [_P, _P, _I64, _I32, _P, _P]),

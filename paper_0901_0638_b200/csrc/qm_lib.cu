@@ -550,6 +550,22 @@ qm_status qm_recycle_exp_to_vg(const void *v, void *x, int64_t n, qm_precision p
     return rode_map_launch(v, x, n, p, table_dev, stream);
 }
 
+qm_status qm_normal_target_table(qm_target kind, const double *params, double *table_dev)
+{
+    if (params == nullptr || table_dev == nullptr || kind != QM_TARGET_STUDENT || !(params[0] > 0.0)) return QM_EINVAL;
+    if (params[0] < QM_RODE_STUDENT_NU_MIN || params[0] > QM_RODE_STUDENT_NU_MAX) return QM_EUNSUPPORTED;
+    std::vector<double> tab(QM_RODE_TABLE_DOUBLES);
+    if (!rode_student_table_build(params[0], tab.data())) return QM_EINVAL;
+    return cudaMemcpy(table_dev, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice) == cudaSuccess
+               ? QM_OK : QM_ECUDA;
+}
+
+qm_status qm_recycle_normal_to_t_rode(const void *z, void *t, int64_t n, qm_precision p, const double *table_dev,
+                                      void *stream)
+{
+    return rode_map_launch(z, t, n, p, table_dev, stream);
+}
+
 qm_status qm_exp_base_quantile(const void *u, void *v, int64_t n, qm_precision p, const double *table_dev,
                                void *stream)
 {

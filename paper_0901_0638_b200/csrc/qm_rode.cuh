@@ -62,6 +62,8 @@ struct RodePrep {
     // uniform segment; on the graded centre segment of a real-lambda VG table
     // (w = Wc (s/n)^4, qm_rode_host.cpp): 4 G s^3 and 12 G s^2, G = Wc/n^4
     double ws0, ws1, wss0, wss1;
+    bool lg;             // segment holds log |R| (Student coarse tail): the value is +-exp(q)
+    bool neg;            // side 1 (v < 0)
 };
 
 // per-side segment boundaries Wc, V and Vmax, held in registers (loaded once
@@ -76,7 +78,16 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
                       __ldg(tab + 28), __ldg(tab + 29)};
 }
 
-template <int M>
+// MODE: the table's features, a kernel-level (warp-uniform) dispatch on the header,
+// so that a plain table pays for neither: bit 0 = graded centre nodes (real-lambda
+// VG, table[32 + 7]), bit 1 = log-valued segment 2 (Student, table[31])
+constexpr int kRodeGraded = 1, kRodeLog = 2;
+QM_DEV int rode_mode(const double *__restrict__ tab)
+{
+    return (__ldg(tab + QM_RODE_SEG + 7) != 0.0 ? kRodeGraded : 0) | (__ldg(tab + 31) != 0.0 ? kRodeLog : 0);
+}
+
+template <int M, int MODE>
 QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double *sm, const RodeBounds &bd)
 {
     const int side = (v < 0.0) ? 1 : 0;
@@ -88,8 +99,8 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     const double2 *r = reinterpret_cast<const double2 *>(sm + QM_RODE_SEG + 24 * side + 8 * j);
     const double2 r01 = r[0], r23 = r[1], r45 = r[2], r67 = r[3];
     double s = (a - r01.x) * r23.x;                             // local coordinate in [0, n]
-    const bool graded = r67.y != 0.0;                           // real-lambda VG centre (r23.x = 1/Wc)
-    if (graded) s = r45.x * sqrt(sqrt(a * r23.x));
+    const bool graded = (MODE & kRodeGraded) && r67.y != 0.0;  // real-lambda VG centre (r23.x = 1/Wc)
+    if (MODE & kRodeGraded) s = graded ? r45.x * sqrt(sqrt(a * r23.x)) : s;
     s = fmin(s, r45.x);
     const double fk = fmin(floor(s), r45.x - 1.0);
     const int k = (int)r23.y + (int)fk;
@@ -105,6 +116,8 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     p.ws1 = graded ? 4.0 * r67.x * k1 * k1 * k1 : r01.y;
     p.wss0 = graded ? 12.0 * r67.x * fk * fk : 0.0;
     p.wss1 = graded ? 12.0 * r67.x * k1 * k1 : 0.0;
+    p.lg = (MODE & kRodeLog) && j == 2;
+    p.neg = side != 0;
     return p;
 }
 
@@ -123,13 +136,14 @@ QM_DEV RodeNodes rode_load(const RodePrep &p)
 }
 
 // quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
+template <int MODE>
 QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
 {
     const double t = p.t;
     // derivatives with respect to s: dR/ds = R' w_s, d2R/ds2 = R'' w_s^2 + R' w_ss
     const double m0 = p.ws0 * n.d0, m1 = p.ws1 * n.d1;
-    const double a0 = __fma_rn(p.ws0 * p.ws0, n.dd0, p.wss0 * n.d0);
-    const double a1 = __fma_rn(p.ws1 * p.ws1, n.dd1, p.wss1 * n.d1);
+    const double a0 = (MODE & kRodeGraded) ? __fma_rn(p.ws0 * p.ws0, n.dd0, p.wss0 * n.d0) : p.ws0 * p.ws0 * n.dd0;
+    const double a1 = (MODE & kRodeGraded) ? __fma_rn(p.ws1 * p.ws1, n.dd1, p.wss1 * n.d1) : p.ws1 * p.ws1 * n.dd1;
     const double dp = n.r1 - n.r0;
     const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
     const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
@@ -137,6 +151,18 @@ QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
     const double q = n.r0 + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
     const double qx = n.r1 + (p.a - p.vmax) * n.d1;             // beyond Vmax: node k+1 = node NT
     return (p.a <= p.vmax) ? q : qx;
+}
+
+// log-valued segment (Student tail, 2e-9 of the normal samples): R = +-exp(q),
+// evaluated only when a lane of the (active) warp needs it
+template <int MODE>
+QM_DEV double rode_unlog(const RodePrep &p, double q)
+{
+    if ((MODE & kRodeLog) && __any_sync(__activemask(), p.lg)) {
+        const double e = exp(q);
+        q = p.lg ? (p.neg ? -e : e) : q;
+    }
+    return q;
 }
 
 // IEEE semantics of the map: +-0 -> +-0, +-inf -> +-inf, NaN -> NaN
@@ -148,7 +174,7 @@ QM_DEV double rode_special(double v, double q)
 
 // B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
 // issued before their arithmetic (4 keeps the state in registers)
-template <int M, int B>
+template <int M, int MODE, int B>
 QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const RodeBounds &bd, const double (&v)[B],
                            double (&x)[B])
 {
@@ -159,11 +185,37 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
         RodePrep p[G];
         RodeNodes nd[G];
 #pragma unroll
-        for (int k = 0; k < G; ++k) p[k] = rode_prep<M>(tab, v[g + k], sm, bd);
+        for (int k = 0; k < G; ++k) p[k] = rode_prep<M, MODE>(tab, v[g + k], sm, bd);
 #pragma unroll
         for (int k = 0; k < G; ++k) nd[k] = rode_load<M>(p[k]);
 #pragma unroll
-        for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_finish(p[k], nd[k]));
+        for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_unlog<MODE>(p[k], rode_finish<MODE>(p[k], nd[k])));
+    }
+}
+
+// kernel-level dispatch on the table's MODE (uniform for the whole grid)
+#define QM_RODE_DISPATCH(tab, CALL)                                                 \
+    switch (rode_mode(tab)) {                                                       \
+    case 0: CALL(0); break;                                                         \
+    case kRodeGraded: CALL(kRodeGraded); break;                                     \
+    case kRodeLog: CALL(kRodeLog); break;                                           \
+    default: CALL(kRodeGraded | kRodeLog); break;                                   \
+    }
+
+template <typename T, int MODE>
+QM_DEV void rode_map_body(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *__restrict__ tab,
+                          const double *rode_sm, const RodeBounds &bd)
+{
+    constexpr int U = 4;
+    const int64_t S = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * S) {
+        double a[U], r[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) a[k] = (i0 + k * S < n) ? (double)v[i0 + k * S] : 0.0;
+        rode_map_batch<kRodeSmemNodes, MODE>(tab, rode_sm, bd, a, r);
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i0 + k * S < n) x[i0 + k * S] = (T)r[k];
     }
 }
 
@@ -174,17 +226,9 @@ k_rode_map(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *
     extern __shared__ __align__(16) double rode_sm[];
     rode_stage_centre(tab, rode_sm);
     const RodeBounds bd = rode_bounds(tab);
-    constexpr int U = 4;
-    const int64_t S = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * S) {
-        double a[U], r[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) a[k] = (i0 + k * S < n) ? (double)v[i0 + k * S] : 0.0;
-        rode_map_batch<kRodeSmemNodes, U>(tab, rode_sm, bd, a, r);
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-            if (i0 + k * S < n) x[i0 + k * S] = (T)r[k];
-    }
+#define QM_RODE_MAP_CALL(MD) rode_map_body<T, MD>(v, x, n, tab, rode_sm, bd)
+    QM_RODE_DISPATCH(tab, QM_RODE_MAP_CALL)
+#undef QM_RODE_MAP_CALL
 }
 
 // the map through the TMA-in / streaming-store pipeline (qm_tma.cuh): the
@@ -194,7 +238,7 @@ template <typename V> struct RodeVec;
 template <> struct RodeVec<double2> { using T = double; static constexpr int W = 2; };
 template <> struct RodeVec<float4> { using T = float; static constexpr int W = 4; };
 
-template <typename V>
+template <typename V, int MODE>
 struct MapRode {
     const double *tab;
     const double *sm;
@@ -208,7 +252,7 @@ struct MapRode {
         double in[PER * W], out[PER * W];
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) in[k] = (double)e[k];
-        rode_map_batch<kRodeTlNodes, PER * W>(tab, sm, bd, in, out);
+        rode_map_batch<kRodeTlNodes, MODE>(tab, sm, bd, in, out);
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) e[k] = (T)out[k];
     }
@@ -221,7 +265,11 @@ k_rode_map_tl(const V *__restrict__ v, V *__restrict__ x, int64_t ntiles, const 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *sm = reinterpret_cast<double *>(smem_raw + kRodeTlTileBytes);
     rode_stage_centre<kRodeTlNodes>(tab, sm);
-    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V>{tab, sm, rode_bounds(tab)});
+    const RodeBounds bd = rode_bounds(tab);
+#define QM_RODE_TL_CALL(MD) \
+    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V, MD>{tab, sm, bd})
+    QM_RODE_DISPATCH(tab, QM_RODE_TL_CALL)
+#undef QM_RODE_TL_CALL
 }
 
 // base quantile Q0: u < p- -> log(u/p-)/(a+b); u > p- -> -log((1-u)/p+)/(a-b).
@@ -251,14 +299,10 @@ k_exp_base_quantile(const T *__restrict__ u, T *__restrict__ v, int64_t n, const
 }
 
 // fused: Philox uniforms (qm_philox_uniform layout) -> Q0 -> Q
-template <typename T>
-__global__ void __launch_bounds__(512, 1)
-k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned long long c0,
-              const double *__restrict__ tab)
+template <typename T, int MODE>
+QM_DEV void rode_philox_body(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned long long c0,
+                             const double *__restrict__ tab, const double *rode_sm, const RodeBounds &bd)
 {
-    extern __shared__ __align__(16) double rode_sm[];
-    rode_stage_centre(tab, rode_sm);
-    const RodeBounds bd = rode_bounds(tab);
     constexpr int W = (sizeof(T) == 4) ? 4 : 2;                 // samples per Philox block
     const int64_t nb = (n + W - 1) / W;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -277,7 +321,7 @@ k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned lo
         }
 #pragma unroll
         for (int k = 0; k < 2 * W; ++k) u[k] = exp_base_quantile(tab, u[k]);
-        rode_map_batch<kRodeSmemNodes, 2 * W>(tab, rode_sm, bd, u, r);
+        rode_map_batch<kRodeSmemNodes, MODE>(tab, rode_sm, bd, u, r);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t b = b0 + h * stride;
@@ -288,6 +332,19 @@ k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned lo
             }
         }
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1)
+k_rode_philox(T *__restrict__ x, int64_t n, unsigned long long seed, unsigned long long c0,
+              const double *__restrict__ tab)
+{
+    extern __shared__ __align__(16) double rode_sm[];
+    rode_stage_centre(tab, rode_sm);
+    const RodeBounds bd = rode_bounds(tab);
+#define QM_RODE_PHILOX_CALL(MD) rode_philox_body<T, MD>(x, n, seed, c0, tab, rode_sm, bd)
+    QM_RODE_DISPATCH(tab, QM_RODE_PHILOX_CALL)
+#undef QM_RODE_PHILOX_CALL
 }
 
 }  // namespace qm

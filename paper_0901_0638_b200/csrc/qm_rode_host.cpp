@@ -434,10 +434,188 @@ bool rode_table_build(int kind, const double *params, double *tab)
     return true;
 }
 
+// ------------------------------------------------ Gaussian base: Student t (§3.6)
+// The "purely numerical method" of P:282-283: the Student Recycling ODE
+// with the Gaussian base (H^(v) = v), solved numerically once per nu
+// and sampled by interpolation.  On the right side (w = v >= 0):
+//     R'' = H(R) R'^2 - w R',   H(R) = (1 + 1/n) R / (1 + R^2/n)
+// and R(-w) = -R(w) (both distributions are symmetric).  Forward from the centre
+// conditions R(0) = 0, R'(0) = gamma the error grows like e^{w^2/2}:
+// the tail equation's neighbours R^-n = A + B erfc(w/sqrt2) saturate,
+// so a relative error e at w leaves e e^{w^2/2}/... at the far tail (the paper's
+// own claim stops at |z| < 6).  As for the exponential base (R30) the table is
+// integrated BACKWARD from an anchor in the far tail, w = 38.5 (beyond the
+// largest |z| a double uniform can give, 38.47), where R is fixed by its
+// definition Fbar_n(R) = Phibar(w): Fbar_n by its convergent large-t series
+//     Fbar_n(t) = k_n n^((n+1)/2) sum_j binom(-(n+1)/2, j) n^j t^-(n+2j) / (n+2j),
+//     k_n = Gamma((n+1)/2) / (sqrt(n pi) Gamma(n/2))     (t^2 > n; Newton in log t),
+// and R' = phi(w)/f_n(R) (the quantile ODE).  In the tail the sweep runs
+// in G = log R (R reaches 1e324 at nu = 1):
+//     G'' = G'^2 n (1 - e^-2G) / (1 + n e^-2G) - w G',
+// which is nearly quadratic (G ~ w^2/(2n)).  Segments: centre [0, 2] (R, forward
+// from the exact centre conditions, 95.4 % of the samples), fine [2, 6] (R),
+// coarse [6, 38.5] in LOG values (G, G', G''), which the kernel exponentiates
+// (table[31] = 1) -- 2e-9 of the samples; beyond 38.5 log-linear extrapolation.
+namespace {
+typedef __float128 f128;
+
+struct StudentRode {
+    ld n;
+    // log k_n, gamma = sqrt(n/2) Gamma(n/2)/Gamma((n+1)/2) (in __float128: lgamma
+    // differences lose the digits of lgamma's size in long double at large n)
+    ld logk, gam;
+    explicit StudentRode(ld nn) : n(nn)
+    {
+        const f128 q = (f128)nn;
+        const f128 lr = lgammaq(q / 2) - lgammaq((q + 1) / 2);           // log Gamma(n/2)/Gamma((n+1)/2)
+        gam = (ld)(sqrtq(q / 2) * expq(lr));
+        logk = (ld)(-lr - 0.5Q * logq(q * M_PIq));
+    }
+    ld H(ld r) const { return (1.0L + 1.0L / n) * r / (1.0L + r * r / n); }
+    // log f_n(t) and log Fbar_n(t) for t^2 >> n
+    ld log_pdf(ld t) const { return logk - 0.5L * (n + 1.0L) * log1pl(t * t / n); }
+    ld log_sf_tail(ld t) const
+    {
+        const ld x = n / (t * t);
+        ld s = 0.0L, c = 1.0L, xp = 1.0L;                                // c = binom(-(n+1)/2, j)
+        for (int j = 0; j < 200; ++j) {
+            const ld term = c * xp / (n + 2.0L * j);
+            s += term;
+            if (fabsl(term) < 1e-22L * fabsl(s)) break;
+            c *= (-(n + 1.0L) / 2.0L - (ld)j) / (ld)(j + 1);
+            xp *= x;
+        }
+        return logk + 0.5L * (n + 1.0L) * logl(n) - n * logl(t) + logl(s);
+    }
+};
+}  // namespace
+
+bool rode_student_table_build(double nu, double *tab)
+{
+    if (!(nu >= QM_RODE_STUDENT_NU_MIN && nu <= QM_RODE_STUDENT_NU_MAX)) return false;
+    const StudentRode T((ld)nu);
+    const ld n = (ld)nu;
+    const int Nc = QM_RODE_CENTRE_NODES, N = QM_RODE_NODES, M = QM_RODE_TAIL_NODES, NT = QM_RODE_NT;
+    const ld Wc = QM_RODE_STUDENT_WC, V = QM_RODE_STUDENT_V, Vmax = QM_RODE_STUDENT_VMAX;
+    std::memset(tab, 0, QM_RODE_HEADER * sizeof(double));
+    // node layout: centre 0..Nc and fine Nc..Nc+N in R (sharing node Nc), coarse
+    // Nc+N+1..NT in log |R| (M - 1 intervals; its first node repeats w = V in log form,
+    // so that no interval mixes linear and log values)
+    const ld w0[3] = {0.0L, Wc, V}, w1[3] = {Wc, V, Vmax};
+    const int k0[3] = {0, Nc, Nc + N + 1}, nseg[3] = {Nc, N, M - 1};
+    ld hs[3];
+    for (int j = 0; j < 3; ++j) hs[j] = (w1[j] - w0[j]) / nseg[j];
+
+    // anchor: Fbar_n(R) = Phibar(Vmax) = erfc(Vmax/sqrt2)/2, Newton in x = log R
+    const ld lp = logl(0.5L * erfcl(Vmax * 0.707106781186547524400844362104849039L));
+    ld x = (T.logk + 0.5L * (n - 1.0L) * logl(n) - lp) / n;             // leading term
+    for (int it = 0; it < 60; ++it) {
+        const ld t = expl(x);
+        const ld g = T.log_sf_tail(t) - lp;
+        const ld dg = -expl(x + T.log_pdf(t) - T.log_sf_tail(t));       // d log Fbar / d log t
+        const ld dx = g / dg;
+        x -= dx;
+        if (fabsl(dx) <= 1e-19L * fabsl(x)) break;
+    }
+    const ld lphi = -0.5L * Vmax * Vmax - 0.918938533204672741780329736405617639L;   // log phi(Vmax)
+    ld G = x, Gp = expl(lphi - T.log_pdf(expl(x)) - x);                  // G' = R'/R = phi/(f R)
+
+    double *nodes = tab + QM_RODE_HEADER;                                // side 0; side 1 = -side 0
+    auto Gpp = [&](ld w, ld g, ld gp) {
+        const ld e = expl(-2.0L * g);
+        return gp * gp * n * (1.0L - e) / (1.0L + n * e) - w * gp;
+    };
+    auto put_log = [&](int k, ld w, ld g, ld gp) {
+        nodes[4 * k] = (double)g; nodes[4 * k + 1] = (double)gp; nodes[4 * k + 2] = (double)Gpp(w, g, gp);
+        nodes[4 * k + 3] = 0.0;
+    };
+    auto put_lin = [&](int k, ld w, ld r, ld rp) {
+        nodes[4 * k] = (double)r; nodes[4 * k + 1] = (double)rp;
+        nodes[4 * k + 2] = (double)(T.H(r) * rp * rp - w * rp); nodes[4 * k + 3] = 0.0;
+    };
+    // classical RK4 (Kahan-compensated state) on y' = F(w, y) for two components
+    ld c0 = 0.0L, c1 = 0.0L;
+    auto acc = [](ld &v, ld &c, ld dv) { const ld y = dv - c, t = v + y; c = (t - v) - y; v = t; };
+    auto rk4 = [&](auto F, ld &a, ld &b, ld w, ld s) {
+        ld k1a, k1b, k2a, k2b, k3a, k3b, k4a, k4b;
+        F(w, a, b, k1a, k1b);
+        F(w + 0.5L * s, a + 0.5L * s * k1a, b + 0.5L * s * k1b, k2a, k2b);
+        F(w + 0.5L * s, a + 0.5L * s * k2a, b + 0.5L * s * k2b, k3a, k3b);
+        F(w + s, a + s * k3a, b + s * k3b, k4a, k4b);
+        acc(a, c0, s / 6.0L * (k1a + 2.0L * k2a + 2.0L * k3a + k4a));
+        acc(b, c1, s / 6.0L * (k1b + 2.0L * k2b + 2.0L * k3b + k4b));
+    };
+    auto Flog = [&](ld w, ld g, ld gp, ld &dg, ld &dgp) { dg = gp; dgp = Gpp(w, g, gp); };
+    auto Flin = [&](ld w, ld r, ld rp, ld &dr, ld &drp) { dr = rp; drp = T.H(r) * rp * rp - w * rp; };
+    const int sub = QM_RODE_SUBSTEPS;
+
+    // backward in G from Vmax down to Wc: coarse nodes in log values, fine nodes in R
+    put_log(NT, Vmax, G, Gp);
+    for (int i = nseg[2] - 1; i >= 0; --i) {
+        const ld wa = w0[2] + (ld)(i + 1) * hs[2];
+        for (int j = 0; j < sub; ++j) rk4(Flog, G, Gp, wa - (ld)j * hs[2] / sub, -hs[2] / sub);
+        put_log(k0[2] + i, w0[2] + (ld)i * hs[2], G, Gp);
+    }
+    put_lin(k0[1] + nseg[1], V, expl(G), Gp * expl(G));
+    for (int i = nseg[1] - 1; i >= 0; --i) {
+        const ld wa = w0[1] + (ld)(i + 1) * hs[1];
+        for (int j = 0; j < sub; ++j) rk4(Flog, G, Gp, wa - (ld)j * hs[1] / sub, -hs[1] / sub);
+        put_lin(k0[1] + i, w0[1] + (ld)i * hs[1], expl(G), Gp * expl(G));
+    }
+    const ld Rc = expl(G), Rpc = Gp * expl(G);                          // backward value at Wc
+    // continue backward in R to w = 0: residual checks Q(0) = 0, Q'(0) = gamma
+    {
+        ld R = Rc, Rp = Rpc;
+        c0 = c1 = 0.0L;
+        for (int k = Nc - 1; k >= 0; --k)
+            for (int i = 0; i < sub; ++i) rk4(Flin, R, Rp, (ld)(k + 1) * hs[0] - (ld)i * hs[0] / sub, -hs[0] / sub);
+        tab[12] = (double)R;
+        tab[14] = (double)(Rp / T.gam - 1.0L);
+    }
+    // centre forward from the exact conditions
+    {
+        ld R = 0.0L, Rp = T.gam;
+        c0 = c1 = 0.0L;
+        put_lin(0, 0.0L, R, Rp);
+        for (int k = 1; k <= Nc; ++k) {
+            for (int i = 0; i < sub; ++i) rk4(Flin, R, Rp, (ld)(k - 1) * hs[0] + (ld)i * hs[0] / sub, hs[0] / sub);
+            if (k < Nc) put_lin(k, (ld)k * hs[0], R, Rp);
+        }
+        tab[22] = (double)(R / Rc - 1.0L);                               // relative joint mismatch at Wc
+    }
+    // side 1: the odd reflection (log values: log |R|, same G', G'')
+    double *left = tab + QM_RODE_HEADER + 4 * (NT + 1);
+    for (int k = 0; k <= NT; ++k) {
+        const bool lg = k >= k0[2];                                      // log |R|: G, G', G'' even
+        left[4 * k] = lg ? nodes[4 * k] : -nodes[4 * k];
+        left[4 * k + 1] = lg ? nodes[4 * k + 1] : -nodes[4 * k + 1];
+        left[4 * k + 2] = lg ? nodes[4 * k + 2] : -nodes[4 * k + 2];
+        left[4 * k + 3] = 0.0;
+    }
+    for (int side = 0; side < 2; ++side) {
+        for (int j = 0; j < 3; ++j) {
+            double *rec = tab + QM_RODE_SEG + 8 * (3 * side + j);
+            rec[0] = (double)w0[j]; rec[1] = (double)hs[j]; rec[2] = (double)(1.0L / hs[j]);
+            rec[3] = k0[j]; rec[4] = nseg[j]; rec[5] = (double)w1[j];
+        }
+        tab[8 + side] = 0.5;
+        tab[10 + side] = 1.0;
+        tab[13] = tab[12]; tab[15] = tab[14]; tab[23] = tab[22];
+        tab[28 + side] = (double)Vmax;
+    }
+    tab[0] = QM_RODE_STUDENT;
+    tab[1] = NT;
+    tab[2] = nu;
+    tab[30] = 3;
+    tab[31] = 1.0;                                                       // segment 2 holds log |R|
+    return true;
+}
+
 }  // namespace qm
 
 // host-side table (diagnostics and the CPU-side tests of the builder)
 extern "C" int qm_rode_table_host(int kind, const double *params, double *table)
 {
+    if (kind == QM_RODE_STUDENT) return (params && qm::rode_student_table_build(params[0], table)) ? 0 : 1;
     return qm::rode_table_build(kind, params, table) ? 0 : 1;
 }

@@ -14,6 +14,7 @@
 // table[12+s] Q(0) residual of the backward sweep           table[14+s] its slope residual
 // table[16+s], table[18+s]: log p_s as hi + lo              table[20+s] 1/rate_s
 // table[22+s] forward/backward mismatch of Q at w = Wc      table[28+s] Vmax_s    table[30] 3
+// table[31] 1 if segment j = 2 holds log |R| (Student), else 0
 // segment record (s, j) at table[32 + 8 (3 s + j)]: w0, h, 1/h, k0, n (intervals), w1, G, graded
 //   graded = 1 only for the centre segment (j = 0) of a real-lambda VG table: its nodes
 //   sit at w_k = Wc (k/n)^4 (G = Wc/n^4, and the 1/h slot holds 1/Wc), so that the
@@ -38,10 +39,21 @@
 #define QM_RODE_VG_MAXM 8                 // integer lambda <= QM_RODE_VG_MAXM + 1: closed-form K_{m+1/2}
 #define QM_RODE_VG_LAMBDA_MIN_REAL 1.1    // non-integer lambda: K_nu of real order, lambda in [1.1, 30]
 #define QM_RODE_VG_LAMBDA_MAX 30.0
+// Gaussian base, Student t (§3.6): kind 3, params {nu}; segments
+// centre [0, 2], fine [2, 6] (R values), coarse [6, 38.5] in log |R| (table[31] = 1;
+// its nodes start at Nc + N + 1, M - 1 intervals), table[2] = nu
+#define QM_RODE_STUDENT 3
+#define QM_RODE_STUDENT_NU_MIN 1.0
+#define QM_RODE_STUDENT_NU_MAX 200.0   // beyond, the anchor series cancels (2.7e-12 at nu = 500)
+#define QM_RODE_STUDENT_WC 2.0L
+#define QM_RODE_STUDENT_V 6.0L
+#define QM_RODE_STUDENT_VMAX 38.5L
 #define QM_RODE_TABLE_LEN (QM_RODE_HEADER + 8 * (QM_RODE_NT + 1))
 
 namespace qm {
 // builds the table in host memory (QM_RODE_TABLE_LEN doubles = QM_RODE_TABLE_DOUBLES of qm.h);
 // false on bad parameters
 bool rode_table_build(int kind, const double *params, double *table);
+// the Student table (kind QM_RODE_STUDENT) for 1 <= nu <= 200; false otherwise
+bool rode_student_table_build(double nu, double *table);
 }  // namespace qm

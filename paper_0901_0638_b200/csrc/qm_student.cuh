@@ -20,6 +20,10 @@
 
 #include "qm_student_params.h"
 
+#ifndef QM_STUDENT_PAIR
+#define QM_STUDENT_PAIR 0   // A/B: 1 = the two samples of a double2 interleaved
+#endif
+
 namespace qm {
 
 QM_DEV double student_central(const StudentParams &sp, double a)
@@ -107,6 +111,20 @@ QM_DEV double student_tail(const StudentParams &sp, double a)
     return (e1.hi == inf) ? inf : t.hi + t.lo;
 }
 
+// the composite from a central value tc already computed for |z|
+QM_DEV double student_finish(const StudentParams &sp, double z, double tc, bool any_tail)
+{
+    const double a = fabs(z);
+    double t = tc;
+    if (any_tail) {
+        const double tt = student_tail(sp, fmax(a, sp.zstar));
+        t = (a >= sp.zstar) ? tt : t;
+    }
+    t = (a == __longlong_as_double(0x7ff0000000000000LL)) ? a : t;
+    const double r = copysign(t, z);
+    return (z == z) ? r : z;
+}
+
 template <int K = 0, int KC = 0>   // K = 0: run-time sp.K / sp.kc
 QM_DEV double student_map(const StudentParams &sp, double z, bool any_tail)
 {
@@ -168,8 +186,21 @@ struct MapStudentF64 {
     template <int PER>
     QM_DEV void map_slice(double2 *a) const
     {
+#if QM_STUDENT_PAIR
+        // the two central series of a double2 in one basic block (two independent
+        // DFMA chains), then the two votes and tails
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const double cx = student_central_k<K, KC>(*sp, fabs(a[j].x));
+            const double cy = student_central_k<K, KC>(*sp, fabs(a[j].y));
+            const bool ax = __any_sync(0xffffffffu, !(fabs(a[j].x) < sp->zstar));
+            const bool ay = __any_sync(0xffffffffu, !(fabs(a[j].y) < sp->zstar));
+            a[j] = make_double2(student_finish(*sp, a[j].x, cx, ax), student_finish(*sp, a[j].y, cy, ay));
+        }
+#else
 #pragma unroll
         for (int j = 0; j < PER; ++j) a[j] = make_double2(one(a[j].x), one(a[j].y));
+#endif
     }
 };
 

@@ -158,7 +158,7 @@ def qm_recycle_exp_to_normal(v: torch.Tensor, out=None, alg: int = BREAKLESS, st
     return z
 
 
-HYPERBOLIC, VG = L.QM_TARGET_HYPERBOLIC, L.QM_TARGET_VG
+HYPERBOLIC, VG, STUDENT = L.QM_TARGET_HYPERBOLIC, L.QM_TARGET_VG, L.QM_TARGET_STUDENT
 
 
 def _params(p):
@@ -172,6 +172,14 @@ def qm_exp_target_table(kind: int, params, device=None) -> torch.Tensor:
     VG: lambda, alpha, beta)."""
     tab = torch.empty(L.QM_RODE_TABLE_DOUBLES, dtype=torch.float64, device=device or "cuda")
     L.check("qm_exp_target_table", L.load().qm_exp_target_table(kind, _params(params), tab.data_ptr()))
+    return tab
+
+
+def qm_normal_target_table(kind: int, params, device=None) -> torch.Tensor:
+    """Device table of the Gaussian-base recycling map solved from the RODE
+    (STUDENT: nu), P:282-283."""
+    tab = torch.empty(L.QM_RODE_TABLE_DOUBLES, dtype=torch.float64, device=device or "cuda")
+    L.check("qm_normal_target_table", L.load().qm_normal_target_table(kind, _params(params), tab.data_ptr()))
     return tab
 
 
@@ -204,6 +212,10 @@ def qm_recycle_exp_to_hyperbolic(v: torch.Tensor, table: torch.Tensor, out=None,
 
 def qm_recycle_exp_to_vg(v: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:
     return _rode_call("qm_recycle_exp_to_vg", v, table, out, stream)
+
+
+def qm_recycle_normal_to_t_rode(z: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return _rode_call("qm_recycle_normal_to_t_rode", z, table, out, stream)
 
 
 def qm_exp_base_quantile(u: torch.Tensor, table: torch.Tensor, out=None, stream=None) -> torch.Tensor:

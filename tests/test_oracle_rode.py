@@ -217,3 +217,74 @@ def test_vg_real_lambda_map_vs_mpmath(par):
         else:
             lhs, rhs = mp.quad(f, [-mp.inf, qq - 1, qq]) / Z, pm * mp.exp((a + b) * vi)
         assert abs(lhs - rhs) / (f(qq) / Z) <= 1e-16 * max(1, abs(qq)), (vi, lhs - rhs)
+
+
+# ------------------------------- Gaussian base: the Student table of §3.6
+def _emulate_kernel(tab, z):
+    """The kernel's interpolation (qm_rode.cuh) in numpy, to check the host table
+    on CPU: segment select, quintic Hermite on (R, R', R''), log segment -> exp."""
+    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    out = np.empty(z.shape)
+    for i, x in enumerate(z):
+        side = 1 if x < 0 else 0
+        a = abs(x)
+        j = int(a >= tab[SEG + 24 * side + 8]) + int(a >= tab[SEG + 24 * side + 16])
+        w0, h, ih, k0, n, w1 = tab[SEG + 24 * side + 8 * j:SEG + 24 * side + 8 * j + 6]
+        s = min((a - w0) * ih, n)
+        fk = min(np.floor(s), n - 1)
+        k, t = int(k0) + int(fk), s - fk
+        nd = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)
+        (r0, d0, e0), (r1, d1, e1) = nd[k, :3], nd[k + 1, :3]
+        m0, m1, a0, a1, dp = h * d0, h * d1, h * h * e0, h * h * e1, r1 - r0
+        c3 = 10 * dp - 6 * m0 - 4 * m1 - 1.5 * a0 + 0.5 * a1
+        c4 = -15 * dp + 8 * m0 + 7 * m1 + 1.5 * a0 - a1
+        c5 = 6 * dp - 3 * m0 - 3 * m1 - 0.5 * a0 + 0.5 * a1
+        q = r0 + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))))
+        if j == 2 and tab[31]:
+            q = -np.exp(q) if side else np.exp(q)
+        out[i] = q
+    return out
+
+
+@pytest.mark.parametrize("nu", [1.0, 3.0, 4.0, 10.0, 200.0])
+def test_product_student_table_vs_oracle(nu):
+    """libqm's Student table (RODE backward from the far-tail anchor, in log t beyond
+    |z| = 2; the centre forward from Q(0) = 0, Q'(0) = gamma): Q(0) and gamma come
+    out as residuals, nodes of every segment equal the oracle's exact map, and the
+    kernel's interpolation (emulated) is within 4e-16 of it on |z| <= 6 -- the
+    paper's numerical solution promises 5e-8 there."""
+    from paper_0901_0638_b200.qm import STUDENT, qm_rode_table_host
+    tab = qm_rode_table_host(STUDENT, [nu])
+    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    assert tab[0] == 3 and tab[1] == NT and tab[31] == 1
+    assert abs(tab[12]) < 1e-15 and abs(tab[14]) < 1e-15 and abs(tab[22]) < 1e-15
+    nodes = tab[H:H + 4 * (NT + 1)].reshape(-1, 4)
+    left = tab[H + 4 * (NT + 1):H + 8 * (NT + 1)].reshape(-1, 4)
+    for j, js in enumerate([[1, 37, 4000], [1, 5000, 16384], [0, 2000, 4094]]):
+        w0, h, ih, k0, n, w1 = tab[SEG + 8 * j:SEG + 8 * j + 6]
+        assert int(k0) == [0, 4096, 4096 + 16384 + 1][j] and abs(w0 + n * h - w1) <= 1e-15 * w1
+        js = np.array(js)
+        ex = O.student_exact(w0 + js * h, nu)
+        got = nodes[int(k0) + js, 0]
+        if j == 2:
+            assert np.max(np.abs(got / np.log(ex).astype(np.float64) - 1)) < 1e-15
+            assert np.array_equal(left[int(k0) + js, :3], nodes[int(k0) + js, :3])   # log |t| is even
+        else:
+            assert np.max(np.abs(got / ex.astype(np.float64) - 1)) < 1e-15
+            assert np.array_equal(left[int(k0) + js, :3], -nodes[int(k0) + js, :3])  # t is odd
+    z = np.concatenate([np.linspace(-6, 6, 401), np.random.default_rng(1).uniform(-38.4, 38.4, 200)])
+    z = z[z != 0]
+    ex = O.student_exact(z, nu).astype(np.float64)
+    g = _emulate_kernel(tab, z)
+    fin = np.isfinite(ex)
+    rel = np.abs(g[fin] / ex[fin] - 1)
+    small = np.abs(z[fin]) <= 6
+    assert rel[small].max() < 4e-16 * 4
+    assert np.all(rel[~small] <= 2e-15 + 4 * 2.0 ** -52 * np.abs(np.log(np.abs(ex[fin][~small]))))
+
+
+def test_product_student_table_rejects():
+    from paper_0901_0638_b200.qm import STUDENT, qm_rode_table_host
+    for nu in (0.5, 0.0, -1.0, 201.0, float("nan")):
+        with pytest.raises(ValueError):
+            qm_rode_table_host(STUDENT, [nu])
