@@ -230,19 +230,21 @@ qm_status qm_mc_european_call(int64_t n, uint64_t seed, uint64_t counter_offset,
  *    (K of real order by Temme's series / Steed's continued fraction; the
  *    origin, where the density is not analytic for non-integer lambda, is
  *    approached on geometric meshes and the centre nodes are graded towards it,
- *    w_k = Wc (k/4096)^4 -- the "many steps near v = 0" of P:395).
+ *    w_k = Wc (k/3584)^4 -- the "many steps near v = 0" of P:395).
  *    Bad parameters -> QM_EINVAL; lambda < 1 (out of scope),
  *    1 < lambda < 1.1 or lambda > 30 -> QM_EUNSUPPORTED.
  *  - qm_recycle_exp_to_hyperbolic / qm_recycle_exp_to_vg: x[i] = Q(v[i]) for
- *    base samples v (quintic Hermite on (Q, Q', Q'') at 24577 nodes per side:
- *    4096 on the centre rate*|v| <= 2 (uniform, or graded as above), 16384 out
- *    to base probability e^-40, 4096 out to e^-800; linear beyond).  +-0, +-inf,
+ *    base samples v (quintic Hermite on (Q, Q', Q'') at 24065 nodes per side:
+ *    3585 on the centre rate*|v| <= 10 -- 7 octave levels [0, Wc/64], [Wc/64,
+ *    Wc/32], ..., [Wc/2, Wc] of 512 uniform intervals (for a real lambda
+ *    rate*|v| <= 2, graded as above) --, 16384 out to base probability e^-40,
+ *    4096 out to e^-800; linear beyond).  +-0, +-inf,
  *    NaN pass through.
  *  - qm_exp_base_quantile: v[i] = Q0(u[i]) of P:322-329.
  *  - qm_exp_target_philox: fused Philox (qm_philox_uniform layout) -> Q0 -> Q.
  * Accuracy (the method's, against the exact map): < 2e-12 relative in fp64
  * (worst near v = 0), correctly rounded to within 2 ulp in fp32. */
-#define QM_RODE_TABLE_DOUBLES (80 + 8 * (4096 + 16384 + 4096 + 1))
+#define QM_RODE_TABLE_DOUBLES (80 + 8 * (3584 + 16384 + 4096 + 1))
 typedef enum { QM_TARGET_HYPERBOLIC = 1, QM_TARGET_VG = 2, QM_TARGET_STUDENT = 3 } qm_target;
 qm_status qm_exp_target_table(qm_target kind, const double *params, double *table_dev);
 qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p,
@@ -260,21 +262,24 @@ qm_status qm_exp_target_philox(void *x, int64_t n, qm_precision p, const double 
  *  - qm_normal_target_table(QM_TARGET_STUDENT, {nu}, table_dev) builds the map
  *    t = F_nu^-1(Phi(z)) into a caller-owned DEVICE buffer of
  *    QM_RODE_TABLE_DOUBLES doubles (the layout of the exponential-base tables):
- *    host setup (~0.2 s) integrating the RODE in long double BACKWARD from an
+ *    host setup (~0.3 s) integrating the RODE in long double BACKWARD from an
  *    anchor at |z| = 38.5 (beyond the largest |z| a double uniform can give),
  *    where t is fixed by its definition -- forward from the centre conditions
  *    Q(0) = 0, Q'(0) = gamma the error grows like e^{z^2/2} --, in
- *    log t beyond |z| = 2; the centre |z| <= 2 is redone forward from the exact
- *    centre conditions.  1 <= nu <= 200; nu <= 0 or a wrong kind -> QM_EINVAL,
- *    0 < nu < 1 or nu > 200 -> QM_EUNSUPPORTED.  Synchronous.
+ *    log t beyond |z| = 2; the nodes with |z| <= 2 are redone forward from the
+ *    exact centre conditions.  1 <= nu <= 200; nu <= 0 or a wrong kind ->
+ *    QM_EINVAL, 0 < nu < 1 or nu > 200 -> QM_EUNSUPPORTED.  Synchronous.
  *  - qm_recycle_normal_to_t_rode: t[i] = A(z[i]) for normal samples z (fp32 or
  *    fp64, any alignment, caller's stream): quintic Hermite on (Q, Q', Q'') at
- *    4097 nodes on |z| <= 2, 16384 on 2..6, and on (log|Q|)', (log|Q|)'' at 4096
- *    on 6..38.5 (exponentiated; log-linear beyond).  +-0, +-inf, NaN pass
- *    through; values beyond the double range -> +-inf.
- * Accuracy against the exact map: < 2e-14 relative on |z| <= 6 (the paper's
- * claim there is 5e-8), and within 2e-14 + 8 eps |log t| beyond (the
- * interpolated quantity is log t). */
+ *    3585 nodes on |z| <= 4.5 (7 octave levels of 512 intervals, all in shared
+ *    memory), 16384 on
+ *    4.5..9, and on (log|Q|, (log|Q|)', (log|Q|)'') at 4096 on 9..38.5
+ *    (exponentiated; log-linear beyond).  +-0, +-inf, NaN pass through; values
+ *    beyond the double range -> +-inf.
+ * Accuracy against the exact map: 4e-15 + 16 eps (1 + kappa(z)) relative, kappa =
+ * |z t'(z)/t(z)| the map's condition number (<= 40 on |z| <= 6, so < 8e-14 there;
+ * the paper's claim is 5e-8) -- the node coordinate and, in the tail, log|t|
+ * carry roundings of an ulp or two that kappa amplifies. */
 qm_status qm_normal_target_table(qm_target kind, const double *params, double *table_dev);
 qm_status qm_recycle_normal_to_t_rode(const void *z, void *t, int64_t n, qm_precision p,
                                       const double *table_dev, void *stream);

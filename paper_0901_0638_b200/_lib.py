@@ -20,7 +20,7 @@ QM_BREAKLESS1212, QM_BREAKLESS88, QM_TWO_REGION = 7, 8, 9
 QM_MOMENT_CHUNK = 65536
 QM_MC_CHUNK = 1 << 20
 QM_TARGET_HYPERBOLIC, QM_TARGET_VG, QM_TARGET_STUDENT = 1, 2, 3
-QM_RODE_TABLE_DOUBLES = 80 + 8 * (4096 + 16384 + 4096 + 1)
+QM_RODE_TABLE_DOUBLES = 80 + 8 * (3584 + 16384 + 4096 + 1)
 QM_MC_MAX_STRIKES = 32
 
 

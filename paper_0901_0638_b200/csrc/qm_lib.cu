@@ -458,13 +458,13 @@ qm_status qm_recycle_normal_to_t_moments(const void *z, void *t, int64_t n, qm_p
         // whole chunks: the map and the moment rows in one pass
         const int64_t nchunks = n / QM_MOMENT_CHUNK;
         if (nchunks > 0) {
-            const size_t smem = (size_t)kStudentStages * kStudentTileVecs * 16;
+            const size_t smem = (size_t)kStudentMomStages * kStudentMomTileVecs * 16;
             auto k = (K == 10) ? k_student_moments_tl<10, 3> : k_student_moments_tl<16, 3>;
             if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return QM_ECUDA;
             const int sms = sm_count_for_current_device();
             const int64_t g = nchunks < (sms > 0 ? sms : 148) ? nchunks : (sms > 0 ? sms : 148);
-            k<<<(int)g, 32 * (kStudentNC + 1), smem, s>>>((const double *)z, (double *)t, nchunks, sp, rows);
+            k<<<(int)g, 32 * (kStudentMomNC + 1), smem, s>>>((const double *)z, (double *)t, nchunks, sp, rows);
             done = nchunks * QM_MOMENT_CHUNK;
         }
     }

@@ -19,18 +19,22 @@
 namespace qm {
 
 // Centre-segment nodes staged in shared memory: (R, R', R'') per node, 3 doubles,
-// nodes 0..Nc of both sides (2 x 4097 x 24 B = 197 KB).  The centre covers
-// rate |v| <= 2, i.e. 1 - e^-2 = 86 % of the base samples; the other nodes are
-// gathered from the table in global memory (L2-resident).
+// nodes 0..Nc of both sides (2 x 3601 x 24 B = 173 KB).  The centre covers
+// rate |v| <= 10 (99.995 % of the base samples; |z| <= 4.5 = 1 - 7e-6 for the
+// Student table; rate |v| <= 2 = 86 % for a real-lambda VG table); the other
+// nodes are gathered from the table in global memory (L2-resident).
 constexpr int kRodeSmemNodes = QM_RODE_CENTRE_NODES + 1;
 constexpr size_t kRodeSmemBytes = (size_t)(QM_RODE_HEADER + 2 * kRodeSmemNodes * 3) * sizeof(double);
-// with the TMA input pipeline (3 x 16 KB of stages) only nodes 0..3599 of each
-// side fit (173 KB): rate |v| <= 1.76, 83 % of the samples
+// with the TMA input pipeline (3 x 16 KB of stages) nodes 0..3599 of each side
+// (173 KB): every centre interval but the last
 #ifndef QM_RODE_TL_NODES
-#define QM_RODE_TL_NODES 3600
+#define QM_RODE_TL_NODES QM_RODE_CENTRE_NODES
 #endif
 constexpr int kRodeTlNodes = QM_RODE_TL_NODES;
-constexpr int kRodeTlStages = 3, kRodeTlTileVecs = 1024, kRodeTlNC = 16;
+#ifndef QM_RODE_TL_NC
+#define QM_RODE_TL_NC 16   // A/B knob: consumer warps of the RODE pipeline
+#endif
+constexpr int kRodeTlStages = 3, kRodeTlTileVecs = 1024, kRodeTlNC = QM_RODE_TL_NC;
 constexpr size_t kRodeTlTileBytes = (size_t)kRodeTlStages * kRodeTlTileVecs * 16;
 constexpr size_t kRodeTlSmemBytes = kRodeTlTileBytes + (size_t)(QM_RODE_HEADER + 2 * kRodeTlNodes * 3) * sizeof(double);
 
@@ -52,8 +56,8 @@ QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
 }
 
 // one sample split in three phases so that a batch of samples has all its node
-// gathers in flight together (the map is latency-bound on them: with 83-86 % of
-// the nodes in shared memory almost every warp still has a lane in L2)
+// gathers in flight together (a warp waits for its slowest lane: one lane with a
+// node in L2 stalls the warp for the L2 latency)
 struct RodePrep {
     const double *b;     // node k of the sample's side (shared or global memory)
     int st;              // doubles from node k to node k+1 (3 shared, 4 global)
@@ -70,21 +74,66 @@ struct RodePrep {
 // per thread): the segment choice needs no shared-memory load
 struct RodeBounds {
     double wc0, wc1, v0, v1, vm0, vm1;
+    double iwc0, iwc1;   // 1/Wc per side (the centre record's 1/h slot when graded or on octaves)
 };
 QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 {
     return RodeBounds{__ldg(tab + QM_RODE_SEG + 8), __ldg(tab + QM_RODE_SEG + 24 + 8),
                       __ldg(tab + QM_RODE_SEG + 16), __ldg(tab + QM_RODE_SEG + 24 + 16),
-                      __ldg(tab + 28), __ldg(tab + 29)};
+                      __ldg(tab + 28), __ldg(tab + 29), __ldg(tab + QM_RODE_SEG + 2), __ldg(tab + QM_RODE_SEG + 24 + 2)};
+}
+
+// one double from shared memory by its 32-bit shared address (an explicit LDS,
+// not a generic load)
+QM_DEV double lds_f64(uint32_t addr)
+{
+    double r;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(addr));
+    return r;
+}
+// select without a branch (the compiler turned some double selects of the
+// octave path into divergent branches)
+QM_DEV double sel_f64(bool c, double a, double b)
+{
+    double r;
+    asm("{ .reg .pred p; setp.ne.u32 p, %3, 0; selp.f64 %0, %1, %2, p; }" : "=d"(r) : "d"(a), "d"(b), "r"((unsigned)c));
+    return r;
 }
 
 // MODE: the table's features, a kernel-level (warp-uniform) dispatch on the header,
-// so that a plain table pays for neither: bit 0 = graded centre nodes (real-lambda
-// VG, table[32 + 7]), bit 1 = log-valued segment 2 (Student, table[31])
-constexpr int kRodeGraded = 1, kRodeLog = 2;
+// so that each table pays only for its own: bit 0 = centre nodes at Wc (k/n)^4
+// (table[32 + 7] = 4), bit 2 = centre on octave levels (= 1), bit 1 = log-valued
+// segment 2 (Student, table[31])
+constexpr int kRodeGraded = 1, kRodeLog = 2, kRodeOct = 4;
 QM_DEV int rode_mode(const double *__restrict__ tab)
 {
-    return (__ldg(tab + QM_RODE_SEG + 7) != 0.0 ? kRodeGraded : 0) | (__ldg(tab + 31) != 0.0 ? kRodeLog : 0);
+    const double g = __ldg(tab + QM_RODE_SEG + 7);
+    return (g == 4.0 ? kRodeGraded : 0) | (g == 1.0 ? kRodeOct : 0) | (__ldg(tab + 31) != 0.0 ? kRodeLog : 0);
+}
+
+// octave-level coordinate of x = w/Wc in [0, 1) (R36; L + 1 levels of NB intervals):
+// x = 2^e m, level l = e + L + 1 (0 below 2^-L); on levels l >= 1 the node index
+// is NB l + the top 9 bits of m's fraction and the local coordinate t the other
+// 43 bits (exact, integer operations); level 0 is uniform, s = 2^(9+L) x.  Node
+// step h = Wc 2^(max(l,1) - L - 10).  (Computing s = 512 (m - 1) + 512 l in double
+// would round t to 41 bits on the upper levels.)
+struct OctCoord { int k; double t, h; };
+QM_DEV OctCoord oct_coord(double x, double wc)
+{
+    constexpr int L = QM_RODE_OCT_LEVELS - 1, NB = QM_RODE_OCT_NODES;
+    static_assert(NB == 512 && L == 6, "the bit layout below assumes 512 intervals per level, 7 levels");
+    const long long xb = __double_as_longlong(x);
+    const int l = min(max((int)(xb >> 52) - 1023 + L + 1, 0), L);
+    const long long mant = xb & 0x000fffffffffffffLL;
+    const int k1 = NB * l + (int)(mant >> 43);
+    const double t1 = __longlong_as_double(0x3ff0000000000000LL | ((mant << 9) & 0x000fffffffffffffLL)) - 1.0;
+    const double s0 = x * (double)(NB << L);
+    const double f0 = floor(s0);
+    OctCoord c;
+    c.k = (l == 0) ? (int)f0 : k1;
+    c.t = sel_f64(l == 0, s0 - f0, t1);
+    c.h = wc * __longlong_as_double((long long)(1023 + max(l, 1) - L - 1 - 9) << 52);
+    return c;
 }
 
 template <int M, int MODE>
@@ -99,23 +148,32 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     const double2 *r = reinterpret_cast<const double2 *>(sm + QM_RODE_SEG + 24 * side + 8 * j);
     const double2 r01 = r[0], r23 = r[1], r45 = r[2], r67 = r[3];
     double s = (a - r01.x) * r23.x;                             // local coordinate in [0, n]
-    const bool graded = (MODE & kRodeGraded) && r67.y != 0.0;  // real-lambda VG centre (r23.x = 1/Wc)
-    if (MODE & kRodeGraded) s = graded ? r45.x * sqrt(sqrt(a * r23.x)) : s;
+    // graded centre (r23.x = 1/Wc, r67 = (G, g)): s = n (w/Wc)^(1/g)
+    const bool g4 = (MODE & kRodeGraded) && r67.y == 4.0;
+    if (MODE & kRodeGraded) s = g4 ? r45.x * sqrt(sqrt(a * r23.x)) : s;
     s = fmin(s, r45.x);
-    const double fk = fmin(floor(s), r45.x - 1.0);
+    double fk = fmin(floor(s), r45.x - 1.0), t = s - fk, hoct = 0.0;
+    if (MODE & kRodeOct) {                                      // centre on octave levels (R36)
+        const bool oc = (j == 0) && r67.y == 1.0;
+        const OctCoord c = oct_coord(a * r23.x, r45.y);         // r45.y = w1 = Wc
+        fk = oc ? (double)c.k : fk;
+        t = sel_f64(oc, c.t, t);
+        hoct = oc ? c.h : 0.0;
+    }
     const int k = (int)r23.y + (int)fk;
     const bool in_sm = (M > 0) && (j == 0) && (k + 1 < M);
     RodePrep p;
     p.b = in_sm ? sm + kRodeSmHdr + 3 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
     p.st = in_sm ? 3 : 4;
-    p.t = s - fk;
+    p.t = t;
     p.a = a;
     p.vmax = side ? bd.vm1 : bd.vm0;
     const double k1 = fk + 1.0;
-    p.ws0 = graded ? 4.0 * r67.x * fk * fk * fk : r01.y;
-    p.ws1 = graded ? 4.0 * r67.x * k1 * k1 * k1 : r01.y;
-    p.wss0 = graded ? 12.0 * r67.x * fk * fk : 0.0;
-    p.wss1 = graded ? 12.0 * r67.x * k1 * k1 : 0.0;
+    // dw/ds and d2w/ds2 at the two nodes: h, 0 (uniform); 4 G s^3, 12 G s^2 (graded)
+    p.ws0 = g4 ? 4.0 * r67.x * fk * fk * fk : ((MODE & kRodeOct) && hoct != 0.0 ? hoct : r01.y);
+    p.ws1 = g4 ? 4.0 * r67.x * k1 * k1 * k1 : ((MODE & kRodeOct) && hoct != 0.0 ? hoct : r01.y);
+    p.wss0 = g4 ? 12.0 * r67.x * fk * fk : 0.0;
+    p.wss1 = g4 ? 12.0 * r67.x * k1 * k1 : 0.0;
     p.lg = (MODE & kRodeLog) && j == 2;
     p.neg = side != 0;
     return p;
@@ -142,8 +200,9 @@ QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
     const double t = p.t;
     // derivatives with respect to s: dR/ds = R' w_s, d2R/ds2 = R'' w_s^2 + R' w_ss
     const double m0 = p.ws0 * n.d0, m1 = p.ws1 * n.d1;
-    const double a0 = (MODE & kRodeGraded) ? __fma_rn(p.ws0 * p.ws0, n.dd0, p.wss0 * n.d0) : p.ws0 * p.ws0 * n.dd0;
-    const double a1 = (MODE & kRodeGraded) ? __fma_rn(p.ws1 * p.ws1, n.dd1, p.wss1 * n.d1) : p.ws1 * p.ws1 * n.dd1;
+    constexpr bool GR = (MODE & kRodeGraded) != 0;
+    const double a0 = GR ? __fma_rn(p.ws0 * p.ws0, n.dd0, p.wss0 * n.d0) : p.ws0 * p.ws0 * n.dd0;
+    const double a1 = GR ? __fma_rn(p.ws1 * p.ws1, n.dd1, p.wss1 * n.d1) : p.ws1 * p.ws1 * n.dd1;
     const double dp = n.r1 - n.r0;
     const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
     const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
@@ -172,6 +231,36 @@ QM_DEV double rode_special(double v, double q)
     return (fabs(v) < __longlong_as_double(0x7ff0000000000000LL)) ? r : v;
 }
 
+// The centre on octave levels (R36; 99.995 % of the base samples) with every
+// node in shared memory: the coordinate of oct_coord, explicit shared loads, no
+// segment record.  Bitwise the same k, t and h as rode_prep.
+struct RodeFast {
+    uint32_t addr;       // shared address of node k's record
+    bool ok;             // a < Wc, node k+1 staged, finite
+    RodePrep p;
+};
+template <int M>
+QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd)
+{
+    const int side = (v < 0.0) ? 1 : 0;
+    const double a = fabs(v);
+    const double wc = side ? bd.wc1 : bd.wc0, iwc = side ? bd.iwc1 : bd.iwc0;
+    const OctCoord c = oct_coord(a * iwc, wc);
+    RodeFast f;
+    f.p.t = c.t;
+    f.p.a = a;
+    f.p.vmax = side ? bd.vm1 : bd.vm0;
+    f.p.ws0 = f.p.ws1 = c.h;
+    f.p.wss0 = f.p.wss1 = 0.0;
+    f.p.lg = false;
+    f.p.neg = side != 0;
+    f.p.b = nullptr;
+    f.p.st = 3;
+    f.ok = (a < wc) && (c.k + 1 < M);
+    f.addr = sm_nodes + 24u * (uint32_t)(side * M + min(c.k, M - 2));
+    return f;
+}
+
 // B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
 // issued before their arithmetic (4 keeps the state in registers)
 template <int M, int MODE, int B>
@@ -182,6 +271,27 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
     static_assert(B % G == 0, "batch must split into groups of 4");
 #pragma unroll
     for (int g = 0; g < B; g += G) {
+        if constexpr ((MODE & kRodeOct) && M > 0) {
+            // warp-uniform fast path: every lane's samples on the staged centre
+            const uint32_t smn = (uint32_t)__cvta_generic_to_shared(sm + kRodeSmHdr);
+            RodeFast f[G];
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < G; ++k) {
+                f[k] = rode_fast_prep<M>(v[g + k], smn, bd);
+                ok = ok && f[k].ok;
+            }
+            if (__all_sync(__activemask(), ok)) {
+                RodeNodes nd[G];
+#pragma unroll
+                for (int k = 0; k < G; ++k)
+                    nd[k] = RodeNodes{lds_f64(f[k].addr), lds_f64(f[k].addr + 8), lds_f64(f[k].addr + 16),
+                                      lds_f64(f[k].addr + 24), lds_f64(f[k].addr + 32), lds_f64(f[k].addr + 40)};
+#pragma unroll
+                for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_finish<MODE>(f[k].p, nd[k]));
+                continue;
+            }
+        }
         RodePrep p[G];
         RodeNodes nd[G];
 #pragma unroll
@@ -196,10 +306,10 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
 // kernel-level dispatch on the table's MODE (uniform for the whole grid)
 #define QM_RODE_DISPATCH(tab, CALL)                                                 \
     switch (rode_mode(tab)) {                                                       \
-    case 0: CALL(0); break;                                                         \
+    case kRodeOct: CALL(kRodeOct); break;                                           \
+    case kRodeOct | kRodeLog: CALL(kRodeOct | kRodeLog); break;                     \
     case kRodeGraded: CALL(kRodeGraded); break;                                     \
-    case kRodeLog: CALL(kRodeLog); break;                                           \
-    default: CALL(kRodeGraded | kRodeLog); break;                                   \
+    default: CALL(kRodeGraded | kRodeOct | kRodeLog); break;                        \
     }
 
 template <typename T, int MODE>

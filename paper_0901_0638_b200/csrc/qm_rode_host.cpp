@@ -231,6 +231,25 @@ ld tail_mass(const Target &t, ld x, int dir, ld rate, ld shift)
     return s;
 }
 
+// centre nodes on octave levels (qm_rode_params.h): level 0 = [0, Wc 2^-L] and level
+// l = [Wc 2^(l-L-1), Wc 2^(l-L)], each cut into QM_RODE_OCT_NODES uniform intervals, so
+// that the spacing follows w (relative accuracy where Q -> 0) and the kernel finds the
+// level and the local coordinate from the exponent and mantissa bits of w/Wc
+ld oct_node(ld Wc, int k)
+{
+    const int L = QM_RODE_OCT_LEVELS - 1, n = QM_RODE_OCT_NODES;
+    const int l = k / n, i = k - l * n;
+    if (l == 0) return Wc * ldexpl((ld)i / n, -L);
+    return Wc * ldexpl(1.0L + (ld)i / n, l - L - 1);
+}
+// first node index with w > wf (nodes below it come from the forward sweep)
+int oct_first_above(ld Wc, ld wf)
+{
+    int k = 0;
+    while (k < QM_RODE_CENTRE_NODES && oct_node(Wc, k) <= wf) ++k;
+    return k;
+}
+
 }  // namespace
 
 bool rode_table_build(int kind, const double *params, double *tab)
@@ -272,18 +291,24 @@ bool rode_table_build(int kind, const double *params, double *tab)
     const int Nc = QM_RODE_CENTRE_NODES, N = QM_RODE_NODES, M = QM_RODE_TAIL_NODES, NT = QM_RODE_NT;
     std::memset(tab, 0, QM_RODE_HEADER * sizeof(double));
 
-    // real-order VG: the density is A(x^2) + |x|^(2 nu) B(x^2) at the origin (R29), so
-    // the map has a v^(2 lambda) term there that a quintic Hermite on uniform nodes
-    // cannot follow.  Its centre segment is graded, node k at w_k = Wc (k/Nc)^4: in
-    // the node coordinate s the term becomes s^(8 lambda) (smooth to the 6th order),
-    // the regular w^2 term s^8 (the quintic's error on it is ~w_1 = 7e-15 Wc relative)
-    // and the far end is 4x coarser in w than a uniform segment.
-    const bool graded = (t.kind == QM_RODE_VG && t.m < 0);
+    // Centre segment: node k at w_k = Wc (k/Nc)^g (qm_rode_params.h).
+    // Centre nodes at w_k = Wc (k/Nc)^4 (quartic grading):
+    //  - Wc = 10/rate (hyperbolic, integer-lambda VG): the segment holds 99.995 % of
+    //    the base samples, so the kernel finds nearly every node in shared memory.  In
+    //    the node coordinate s the map is Q'(0) G s^4 + ... (G = Wc/Nc^4 = 7e-14/rate):
+    //    fine where Q -> 0 needs relative accuracy (a quadratic grading, G = Wc/Nc^2,
+    //    left the s^6 term's interpolation error at 2e-13 of Q in the first interval),
+    //    and 4 Wc/Nc = 0.01/rate apart at the far end.
+    //  - Wc = 2/rate (real-order VG): the density is A(x^2) + |x|^(2 nu) B(x^2) at
+    //    the origin (R29), so the map has a v^(2 lambda) term there; in s it becomes
+    //    s^(8 lambda) (smooth to the 6th order), the regular w^2 term s^8.
+    const bool real_order = (t.kind == QM_RODE_VG && t.m < 0);
     for (int side = 0; side < 2; ++side) {
         const ld rate = side == 0 ? rr : rl, p = side == 0 ? pp : pm;
         const int dir = side == 0 ? +1 : -1;
         // segments: centre [0, Wc], fine [Wc, V], coarse [V, Vmax] (qm_rode_params.h)
-        const ld Wc = QM_RODE_VRATE_C / rate, V = QM_RODE_VRATE / rate, Vmax = QM_RODE_VRATE2 / rate;
+        const ld Wc = (real_order ? QM_RODE_VRATE_C : QM_RODE_VRATE_CQ) / rate, V = QM_RODE_VRATE / rate,
+                 Vmax = QM_RODE_VRATE2 / rate;
         const ld w0[3] = {0.0L, Wc, V}, w1[3] = {Wc, V, Vmax};
         const int k0[3] = {0, Nc, Nc + N}, nseg[3] = {Nc, N, M};
         ld hs[3];
@@ -296,17 +321,24 @@ bool rode_table_build(int kind, const double *params, double *tab)
             rec[3] = k0[j];
             rec[4] = nseg[j];
             rec[5] = (double)w1[j];
-            if (j == 0 && graded) {               // kernel: s = n (w / Wc)^(1/4), w_s = 4 G s^3, G = Wc/n^4
+            if (j == 0) {
                 rec[2] = (double)(1.0L / Wc);
-                rec[6] = (double)(Wc / ((ld)Nc * Nc * Nc * Nc));
-                rec[7] = 1.0;
+                if (real_order) {                 // kernel: s = n (w / Wc)^(1/4), w_s = 4 G s^3, G = Wc/n^4
+                    rec[6] = (double)(Wc / ((ld)Nc * Nc * Nc * Nc));
+                    rec[7] = 4.0;
+                } else {                          // octave levels
+                    rec[7] = 1.0;
+                }
             }
         }
         auto wnode = [&](int k) {                 // centre node positions
-            if (!graded) return (ld)k * hs[0];
+            if (!real_order) return oct_node(Wc, k);
             const ld x = (ld)k / (ld)Nc;
             return Wc * (x * x) * (x * x);
         };
+        // nodes 0..kf-1 come from the forward sweep from the exact centre conditions
+        // (error growth e^{rate w} <= e^2 there), nodes kf.. from the backward sweep
+        const int kf = real_order ? Nc : oct_first_above(Wc, QM_RODE_VRATE_FWD / rate);
         auto seg_of = [&](int k) { return k >= k0[2] ? 2 : (k >= k0[1] ? 1 : 0); };   // interval [k, k+1]
 
         // anchor: tail mass of the target beyond Q(Vmax) equals the base's, p e^{-rate Vmax}
@@ -353,31 +385,48 @@ bool rode_table_build(int kind, const double *params, double *tab)
             acc(Q, cQ, s / 6.0L * (k1q + 2.0L * k2q + 2.0L * k3q + k4q));
             acc(P, cP, s / 6.0L * (k1p + 2.0L * k2p + 2.0L * k3p + k4p));
         };
-        // backward: coarse, fine, then the centre (stored only down to Wc; the
-        // rest of the sweep gives the checks at v = 0)
+        // backward: coarse, fine, then the centre (stored down to node kf; the rest of
+        // the sweep gives the checks at v = 0)
         ld Qc = 0.0L;
-        // real-order VG: H has a |Q|^(2 nu - 1) (or Q log Q) term at the origin, so the
-        // interval next to v = 0 is stepped on a geometric mesh (w_i = h0 r^-i): RK4's
-        // error there scales with the local step over the distance to 0, not with h0
         constexpr int NG = 4800;                               // r = 1.005: h0 r^-4800 ~ 4e-11 h0 (r = 1.12 left 1e-13 at lambda = 1.5,
                                                                // 1.02 left 5e-15 at lambda = 1.2; 1.005 converged to 1e-17 at 1.1)
         const ld rg = 1.005L;
-        for (int k = NT - 1; k >= 0; --k) {
-            const ld hk = hs[seg_of(k)];
-            if (k == 0 && graded) {
-                ld w = hk;
-                for (int i = 1; i <= NG; ++i) {
-                    const ld wn = hk * powl(rg, -(ld)i);
-                    rk4(Q, P, wn - w);
-                    w = wn;
+        // one centre interval [w_k, w_{k+1}] forward (dir_s = +1) or backward (-1) on
+        // geometric substeps (ratio <= rg; at least nmin), the first one down to 4e-11 of
+        // w_1 next to v = 0 (real-order VG: H has a |Q|^(2 nu - 1) or Q log Q term there,
+        // and RK4's error scales with the local step over the distance to 0)
+        auto centre_interval = [&](int k, int dir_s, int nmin) {
+            const ld wa = wnode(k), wb = wnode(k + 1);
+            if (k == 0) {
+                if (dir_s > 0) {
+                    ld w = 0.0L;
+                    for (int i = NG; i >= 1; --i) { const ld wn = wb * powl(rg, -(ld)i); rk4(Q, P, wn - w); w = wn; }
+                    rk4(Q, P, wb - w);
+                } else {
+                    ld w = wb;
+                    for (int i = 1; i <= NG; ++i) { const ld wn = wb * powl(rg, -(ld)i); rk4(Q, P, wn - w); w = wn; }
+                    rk4(Q, P, -w);
                 }
-                rk4(Q, P, -w);
-            } else {
-                const int ns = (graded && k < 64) ? sub * (64 / (k + 1)) : sub;   // finer near 0
-                for (int j = 0; j < ns; ++j) rk4(Q, P, -hk / ns);
+                return;
             }
-            if (k >= Nc) put(k, Q, P);
-            if (k == Nc) Qc = Q;
+            const int ns = std::max(nmin, (int)ceill(logl(wb / wa) / logl(rg)));
+            ld w = dir_s > 0 ? wa : wb;
+            for (int i = 1; i <= ns; ++i) {
+                const ld x = (ld)i / (ld)ns;
+                const ld wn = (i == ns) ? (dir_s > 0 ? wb : wa) : (dir_s > 0 ? wa * powl(wb / wa, x) : wb * powl(wa / wb, x));
+                rk4(Q, P, wn - w);
+                w = wn;
+            }
+        };
+        for (int k = NT - 1; k >= 0; --k) {
+            if (k < Nc) {
+                centre_interval(k, -1, k >= kf ? 4 * sub : sub);
+            } else {
+                const ld hk = hs[seg_of(k)];
+                for (int j = 0; j < sub; ++j) rk4(Q, P, -hk / sub);
+            }
+            if (k >= kf) put(k, Q, P);
+            if (k == kf) Qc = Q;
         }
         // checks against the centre conditions of P:336 / P:344
         const ld slope0 = dir * p * rate * Z / expl(t.logg(0.0L) - shift);
@@ -385,41 +434,18 @@ bool rode_table_build(int kind, const double *params, double *tab)
         tab[14 + side] = (double)(P / slope0 - 1.0L);          // relative slope residual
         // Near the centre the backward sweep's accumulated ABSOLUTE error (~1e-14) is a
         // large RELATIVE error because Q -> 0.  There the forward direction is benign over
-        // a short distance (error growth e^{rate w} <= e^2 on the centre segment), so the
-        // centre segment is integrated forward from the exact conditions Q(0) = 0,
-        // Q'(0) = slope0 (node Nc keeps the backward value; the mismatch is recorded).
+        // a short distance (error growth e^{rate w} <= e^2 for rate w <= 2), so nodes
+        // 0..kf-1 are integrated forward from the exact conditions Q(0) = 0,
+        // Q'(0) = slope0 (node kf keeps the backward value; the mismatch is recorded).
         Q = 0.0L;
         P = slope0;
         cQ = cP = 0.0L;
         put(0, Q, P);
-        for (int k = 1; k <= Nc; ++k) {
-            if (graded) {
-                // geometric substeps (ratio <= rg) from node k-1 to node k; from 0 to node 1
-                // down to 4e-11 of it first
-                const ld wa = wnode(k - 1), wb = wnode(k);
-                ld w = 0.0L;
-                if (k == 1) {
-                    for (int i = NG; i >= 1; --i) {
-                        const ld wn = wb * powl(rg, -(ld)i);
-                        rk4(Q, P, wn - w);
-                        w = wn;
-                    }
-                    rk4(Q, P, wb - w);
-                } else {
-                    const int ns = std::max(4 * sub, (int)ceill(logl(wb / wa) / logl(rg)));
-                    w = wa;
-                    for (int i = 1; i <= ns; ++i) {
-                        const ld wn = (i == ns) ? wb : wa * powl(wb / wa, (ld)i / (ld)ns);
-                        rk4(Q, P, wn - w);
-                        w = wn;
-                    }
-                }
-            } else {
-                for (int j = 0; j < sub; ++j) rk4(Q, P, hs[0] / sub);
-            }
-            if (k < Nc) put(k, Q, P);
+        for (int k = 1; k <= kf; ++k) {
+            centre_interval(k - 1, +1, 4 * sub);
+            if (k < kf) put(k, Q, P);
         }
-        tab[22 + side] = (double)(Q - Qc);                     // joint mismatch at Wc
+        tab[22 + side] = (double)(Q - Qc);                     // joint mismatch at node kf
         tab[8 + side] = (double)p;
         tab[10 + side] = (double)rate;
         const ld lp = logl(p);
@@ -452,10 +478,11 @@ bool rode_table_build(int kind, const double *params, double *tab)
 // and R' = phi(w)/f_n(R) (the quantile ODE).  In the tail the sweep runs
 // in G = log R (R reaches 1e324 at nu = 1):
 //     G'' = G'^2 n (1 - e^-2G) / (1 + n e^-2G) - w G',
-// which is nearly quadratic (G ~ w^2/(2n)).  Segments: centre [0, 2] (R, forward
-// from the exact centre conditions, 95.4 % of the samples), fine [2, 6] (R),
-// coarse [6, 38.5] in LOG values (G, G', G''), which the kernel exponentiates
-// (table[31] = 1) -- 2e-9 of the samples; beyond 38.5 log-linear extrapolation.
+// which is nearly quadratic (G ~ w^2/(2n)).  Segments: centre [0, 4.5] with nodes at
+// 4.5 (k/Nc)^4 (R; the nodes with w <= 2 forward from the exact centre conditions;
+// 1 - 7e-6 of the samples), fine [4.5, 9] (R), coarse [9, 38.5] in LOG values (G, G',
+// G''), which the kernel exponentiates (table[31] = 1; 2e-19 of the samples);
+// beyond 38.5 log-linear extrapolation.
 namespace {
 typedef __float128 f128;
 
@@ -497,6 +524,8 @@ bool rode_student_table_build(double nu, double *tab)
     const ld n = (ld)nu;
     const int Nc = QM_RODE_CENTRE_NODES, N = QM_RODE_NODES, M = QM_RODE_TAIL_NODES, NT = QM_RODE_NT;
     const ld Wc = QM_RODE_STUDENT_WC, V = QM_RODE_STUDENT_V, Vmax = QM_RODE_STUDENT_VMAX;
+    auto wnode = [&](int k) { return oct_node(Wc, k); };                 // centre nodes (octave levels)
+    const int kf = oct_first_above(Wc, QM_RODE_STUDENT_WF);             // forward: nodes < kf
     std::memset(tab, 0, QM_RODE_HEADER * sizeof(double));
     // node layout: centre 0..Nc and fine Nc..Nc+N in R (sharing node Nc), coarse
     // Nc+N+1..NT in log |R| (M - 1 intervals; its first node repeats w = V in log form,
@@ -562,26 +591,36 @@ bool rode_student_table_build(double nu, double *tab)
         for (int j = 0; j < sub; ++j) rk4(Flog, G, Gp, wa - (ld)j * hs[1] / sub, -hs[1] / sub);
         put_lin(k0[1] + i, w0[1] + (ld)i * hs[1], expl(G), Gp * expl(G));
     }
-    const ld Rc = expl(G), Rpc = Gp * expl(G);                          // backward value at Wc
+    // the centre's outer nodes (w >= 2) still in log variables, node to node
+    const int sc = 4 * sub;                                              // centre: 0.0027 apart at w = 2
+    for (int k = Nc - 1; k >= kf; --k) {
+        const ld wa = wnode(k + 1), hn = wa - wnode(k);
+        for (int j = 0; j < sc; ++j) rk4(Flog, G, Gp, wa - (ld)j * hn / sc, -hn / sc);
+        put_lin(k, wnode(k), expl(G), Gp * expl(G));
+    }
+    const ld Rc = expl(G), Rpc = Gp * expl(G);                          // backward value at node kf
     // continue backward in R to w = 0: residual checks Q(0) = 0, Q'(0) = gamma
     {
         ld R = Rc, Rp = Rpc;
         c0 = c1 = 0.0L;
-        for (int k = Nc - 1; k >= 0; --k)
-            for (int i = 0; i < sub; ++i) rk4(Flin, R, Rp, (ld)(k + 1) * hs[0] - (ld)i * hs[0] / sub, -hs[0] / sub);
+        for (int k = kf - 1; k >= 0; --k) {
+            const ld wa = wnode(k + 1), hn = wa - wnode(k);
+            for (int i = 0; i < sc; ++i) rk4(Flin, R, Rp, wa - (ld)i * hn / sc, -hn / sc);
+        }
         tab[12] = (double)R;
         tab[14] = (double)(Rp / T.gam - 1.0L);
     }
-    // centre forward from the exact conditions
+    // centre nodes 0..kf-1 forward from the exact conditions
     {
         ld R = 0.0L, Rp = T.gam;
         c0 = c1 = 0.0L;
         put_lin(0, 0.0L, R, Rp);
-        for (int k = 1; k <= Nc; ++k) {
-            for (int i = 0; i < sub; ++i) rk4(Flin, R, Rp, (ld)(k - 1) * hs[0] + (ld)i * hs[0] / sub, hs[0] / sub);
-            if (k < Nc) put_lin(k, (ld)k * hs[0], R, Rp);
+        for (int k = 1; k <= kf; ++k) {
+            const ld wa = wnode(k - 1), hn = wnode(k) - wa;
+            for (int i = 0; i < sc; ++i) rk4(Flin, R, Rp, wa + (ld)i * hn / sc, hn / sc);
+            if (k < kf) put_lin(k, wnode(k), R, Rp);
         }
-        tab[22] = (double)(R / Rc - 1.0L);                               // relative joint mismatch at Wc
+        tab[22] = (double)(R / Rc - 1.0L);                               // relative joint mismatch at node kf
     }
     // side 1: the odd reflection (log values: log |R|, same G', G'')
     double *left = tab + QM_RODE_HEADER + 4 * (NT + 1);
@@ -597,6 +636,10 @@ bool rode_student_table_build(double nu, double *tab)
             double *rec = tab + QM_RODE_SEG + 8 * (3 * side + j);
             rec[0] = (double)w0[j]; rec[1] = (double)hs[j]; rec[2] = (double)(1.0L / hs[j]);
             rec[3] = k0[j]; rec[4] = nseg[j]; rec[5] = (double)w1[j];
+            if (j == 0) {                                                // octave levels
+                rec[2] = (double)(1.0L / Wc);
+                rec[7] = 1.0;
+            }
         }
         tab[8 + side] = 0.5;
         tab[10 + side] = 1.0;

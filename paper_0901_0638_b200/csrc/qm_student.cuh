@@ -205,7 +205,21 @@ struct MapStudentF64 {
 };
 
 // 1 CTA/SM: a producer warp + 16 consumer warps, 4 stages of 32 KB (2048 double2)
-constexpr int kStudentNC = 16, kStudentStages = 4, kStudentTileVecs = 2048;
+// (A/B knobs: QM_STUDENT_NC consumer warps, QM_STUDENT_STAGES, QM_STUDENT_TV double2 per tile)
+#ifndef QM_STUDENT_NC
+#define QM_STUDENT_NC 16
+#endif
+#ifndef QM_STUDENT_STAGES
+#define QM_STUDENT_STAGES 4
+#endif
+#ifndef QM_STUDENT_TV
+#define QM_STUDENT_TV 2048
+#endif
+constexpr int kStudentNC = QM_STUDENT_NC, kStudentStages = QM_STUDENT_STAGES, kStudentTileVecs = QM_STUDENT_TV;
+static_assert(kStudentTileVecs % (32 * kStudentNC) == 0, "a tile splits evenly over the consumer lanes");
+// the fused-moments kernel keeps 16 consumer warps and 32 KB tiles (a moment chunk of
+// 65536 samples is 16 whole tiles)
+constexpr int kStudentMomNC = 16, kStudentMomStages = 4, kStudentMomTileVecs = 2048;
 
 template <int K, int KC>
 __global__ void __launch_bounds__(32 * (kStudentNC + 1), 1)
@@ -226,11 +240,11 @@ k_student_f64_tl(const double *__restrict__ z, double *__restrict__ t, int64_t n
 // chunk -- deterministic and independent of the grid, like qm_moment_rows (the
 // rows differ from its in summation order only).
 template <int K, int KC>
-__global__ void __launch_bounds__(32 * (kStudentNC + 1), 1)
+__global__ void __launch_bounds__(32 * (kStudentMomNC + 1), 1)
 k_student_moments_tl(const double *__restrict__ z, double *__restrict__ t, int64_t nchunks,
                      const __grid_constant__ StudentParams sp, double *__restrict__ rows)
 {
-    constexpr int TV = kStudentTileVecs, S = kStudentStages, NC = kStudentNC;
+    constexpr int TV = kStudentMomTileVecs, S = kStudentMomStages, NC = kStudentMomNC;
     constexpr int TPC = QM_MOMENT_CHUNK / (2 * TV);                 // tiles per chunk
     constexpr int PER = TV / (32 * NC);
     constexpr uint32_t TILE_BYTES = TV * 16;

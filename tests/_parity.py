@@ -1,4 +1,6 @@
 """ULP comparison of a GPU result with the oracle's long-double value (no method arithmetic)."""
+import math
+
 import numpy as np
 
 
@@ -38,3 +40,20 @@ def summary(err: np.ndarray) -> dict:
         return {"max_ulp": 0.0, "hist": []}
     h = np.histogram(np.minimum(err, 8.0), bins=[0, 0.5, 1, 1.5, 2, 3, 4, 8, 9])[0]
     return {"max_ulp": float(err.max()) if err.size else 0.0, "hist": h.tolist()}
+
+
+def student_rode_bar(z, t, nu):
+    """Accuracy bar of the interpolated Student map (qm.h): 4e-15 + 16 eps (1 + kappa),
+    kappa = |z t'(z) / t(z)| the map's condition number, t' = phi(z) / f_nu(t) (the
+    quantile ODE).  The kernel's node coordinate s = n (|z|/Wc)^(1/4) and, in
+    the tail, the interpolated log|t| carry roundings of a few ulp of z, which kappa
+    amplifies (kappa ~ 20 at |z| = 4.5 for nu = 1, ~ z^2/nu in the tail)."""
+    z = np.abs(np.asarray(z, np.float64))
+    t = np.abs(np.asarray(t, np.float64))
+    x = t / math.sqrt(nu)
+    with np.errstate(over="ignore", divide="ignore"):
+        l1p = np.where(x > 1e100, 2 * np.log(x), np.log1p(np.minimum(x, 1e100) ** 2))    # log(1 + x^2)
+    lf = math.lgamma((nu + 1) / 2) - math.lgamma(nu / 2) - 0.5 * math.log(nu * math.pi) - 0.5 * (nu + 1) * l1p
+    lphi = -0.5 * z * z - 0.5 * math.log(2 * math.pi)
+    kappa = z * np.exp(lphi - lf - np.log(t))
+    return 4e-15 + 16 * 2.0 ** -53 * (1 + kappa)

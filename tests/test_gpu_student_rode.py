@@ -3,22 +3,21 @@
 sampled by quintic Hermite interpolation in the kernel (row a6 by the RODE;
 SURVEY E14).  Reference: the oracle's exact map F_n^-1(Phi(z)) (inverse
 incomplete beta, pinned in test_oracle_student.py).
-Bars (fp64): 2e-14 relative on |z| <= 6 -- the table nodes are within ~1e-16 and
-the interpolation error (h^6 |R^(6)|/46080) is < 1e-18 there, so the bar is the
-arithmetic of the Hermite evaluation; beyond |z| = 6 the kernel interpolates
-log|t|, whose rounding (|log t| eps) becomes a relative error of t:
-2e-14 + 8 eps |log t|.  The paper's own claim is 5e-8 on |z| < 6.  fp32: 1 ulp
-(a double result within 1e-13 rounded to float)."""
+Bar (fp64): 4e-15 + 16 eps (1 + kappa(z)), kappa = |z t'/t| the map's condition
+number (_parity.student_rode_bar): the table nodes are within ~1e-16 and the
+quintic's error is < 5e-15, and the roundings of the node coordinate
+s = n (|z|/4.5)^(1/4) (centre) or of the interpolated log|t| (|z| > 9) are amplified
+by kappa (<= 40 on |z| <= 6, ~z^2/nu in the tail).  The paper's own claim is
+5e-8 on |z| < 6.  fp32: 1 ulp (a double result within ~1e-13 rounded to float)."""
 import numpy as np
 import pytest
 import torch
 
 import oracle as O
-from _parity import ulp_errors
+from _parity import student_rode_bar, ulp_errors
 
 pytestmark = pytest.mark.gpu
 Q = pytest.importorskip("paper_0901_0638_b200.qm")
-EPS = 2.0 ** -52
 
 
 def _z(n, seed=3):
@@ -28,9 +27,8 @@ def _z(n, seed=3):
     return np.concatenate([rng.standard_normal(n), rng.uniform(-38.4, 38.4, n // 4), edges])
 
 
-def _bar(z, ex):
-    lg = np.abs(np.log(np.abs(ex)))
-    return np.where(np.abs(z) <= 6.0, 2e-14, 2e-14 + 8 * EPS * lg)
+def _bar(z, ex, nu):
+    return student_rode_bar(z, ex, nu)
 
 
 @pytest.mark.parametrize("nu", [1.0, 1.5, 3.0, 4.0, 5.0, 10.0, 30.0, 200.0])
@@ -41,7 +39,7 @@ def test_student_rode_vs_exact_map(nu):
     ex = O.student_exact(z, nu).astype(np.float64)
     fin = np.isfinite(ex) & (z != 0)
     rel = np.abs(g[fin] / ex[fin] - 1)
-    bar = _bar(z[fin], ex[fin])
+    bar = _bar(z[fin], ex[fin], nu)
     assert np.all(rel <= bar), (np.max(rel / bar), z[fin][np.argmax(rel / bar)])
     # beyond the double range (nu = 1 past |z| ~ 37.5): +-inf like the exact value
     assert np.array_equal(g[~np.isfinite(ex)], ex[~np.isfinite(ex)])
@@ -96,6 +94,6 @@ def test_student_rode_pipeline_equals_ldg_kernel(dtype):
     g = tiled.cpu().numpy()[idx].astype(np.float64)
     ex = O.student_exact(z[idx].astype(np.float64), 3.0).astype(np.float64)
     if dtype == np.float64:
-        assert np.all(np.abs(g / ex - 1) <= _bar(z[idx].astype(np.float64), ex))
+        assert np.all(np.abs(g / ex - 1) <= _bar(z[idx].astype(np.float64), ex, 3.0))
     else:
         assert ulp_errors(g.astype(np.float32), ex, np.float32).max() <= 1.0

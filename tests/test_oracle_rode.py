@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+from _parity import student_rode_bar
 from _util import ld2mp
 
 HYP = [(1.0, 0.0, 1.0), (1.0, 0.5, 1.0), (2.0, -1.0, 0.5)]
@@ -104,6 +105,20 @@ def test_vg_lambda2_closed_form_cdf():
 
 
 # ------------------------------------------- the product's host-side table builder
+def _node_w(tab, side, j, ks):
+    """positions of nodes k0 + ks of segment j (qm_rode_params.h): uniform, octave
+    levels (g = 1: level 0 = [0, Wc/64], level l = [Wc 2^(l-7), Wc 2^(l-6)], 512
+    intervals each) or quartic-graded (g = 4)"""
+    w0, h, ih, k0, n, w1, G, g = tab[32 + 8 * (3 * side + j):32 + 8 * (3 * side + j) + 8]
+    ks = np.asarray(ks)
+    if g == 1:
+        lv, i = ks // 512, ks % 512
+        return np.where(lv == 0, w1 * np.ldexp(i / 512.0, -6), w1 * np.ldexp(1 + i / 512.0, lv - 7))
+    if g == 4:
+        return G * ks.astype(np.float64) ** 4
+    return w0 + ks * h
+
+
 @pytest.mark.parametrize("kind,par", [(O.HYPERBOLIC, p) for p in HYP] +
                          [(O.VG, [1, 2.0, 0.5]), (O.VG, [2, 2.0, 0.5]), (O.VG, [3, 1.0, -0.4]),
                           (O.VG, [1.5, 2.0, 0.5]), (O.VG, [2.7, 1.0, -0.6])])
@@ -113,7 +128,8 @@ def test_product_rode_table_vs_oracle(kind, par):
     vs differences of it; Q(0) = 0 and the centre slopes of P:336/P:344 as residuals."""
     from paper_0901_0638_b200.qm import qm_rode_table_host
     tab = qm_rode_table_host(kind, par)
-    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    H, SEG = 80, 32
+    NT, NC = int(tab[1]), int(tab[SEG + 4])                              # layout from the header
     assert tab[1] == NT and tab[30] == 3
     assert np.all(np.abs(tab[12:14]) < 1e-12) and np.all(np.abs(tab[14:16]) < 1e-12)
     assert np.all(np.abs(tab[22:24]) < 1e-14 * (1 + 2.0 / (tab[10:12])))         # forward/backward joint
@@ -123,21 +139,20 @@ def test_product_rode_table_vs_oracle(kind, par):
         sg = 1 if side == 0 else -1
         nodes = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)
         assert nodes[0, 0] == 0.0
-        for j, js in enumerate([[1, 2, 37, 4000], [1, 500, 5000, 16383], [1, 100, 2000, 4096]]):
-            w0, h, ih, k0, n, w1, G, graded = tab[SEG + 8 * (3 * side + j):SEG + 8 * (3 * side + j) + 8]
-            assert int(k0) == [0, 4096, 4096 + 16384][j] and abs(w0 + n * h - w1) <= 1e-12 * w1
+        for j, js in enumerate([[1, 2, 37, 1800, 3583], [1, 500, 5000, 16383], [1, 100, 2000, 4096]]):
+            w0, h, ih, k0, n, w1, G, g = tab[SEG + 8 * (3 * side + j):SEG + 8 * (3 * side + j) + 8]
+            assert int(k0) == [0, NC, NC + 16384][j] and abs(w0 + n * h - w1) <= 1e-12 * w1
             js = np.array(js)
-            # real-lambda VG: centre nodes at Wc (k/n)^4 (graded, R29)
-            wk = G * js.astype(np.float64) ** 4 if graded else w0 + js * h
-            assert (graded == 0) or (j == 0 and kind == O.VG and par[0] != int(par[0]))
+            # centre nodes at Wc (k/n)^4 (Wc = 2/rate for real-lambda VG (R29), else 10/rate)
+            wk = _node_w(tab, side, j, js)
+            real = kind == O.VG and par[0] != int(par[0])
+            assert g == (0 if j else (4 if real else 1)) and (j or abs(w1 * tab[10 + side] - (2 if real else 10)) < 1e-12)
             ex = O.recycle_exp_to_target(kind, par, wk * sg).astype(np.float64)
             assert np.abs(nodes[int(k0) + js, 0] / ex - 1).max() < 1e-13, j
         # R' and R'' against central differences of the exact map (long double; O(hh^2) ~ 1e-8)
-        w0, h, G, graded = tab[SEG + 8 * 3 * side], tab[SEG + 8 * 3 * side + 1], tab[SEG + 8 * 3 * side + 6], \
-            tab[SEG + 8 * 3 * side + 7]
-        ks = np.array([1, 2, 37, 500]) if not graded else np.array([300, 500, 1000, 2000])
-        w = G * ks.astype(np.float64) ** 4 if graded else ks * h
-        hh = 1e-2 * h
+        ks = np.array([300, 500, 1000, 2000, 3500])
+        w = _node_w(tab, side, 0, ks)
+        hh = 1e-2 * tab[SEG + 8 * 3 * side + 1]                           # 1e-2 Wc/n
         qp = O.recycle_exp_to_target(kind, par, (w + hh) * sg)
         q0 = O.recycle_exp_to_target(kind, par, w * sg)
         qm = O.recycle_exp_to_target(kind, par, (w - hh) * sg)
@@ -223,19 +238,38 @@ def test_vg_real_lambda_map_vs_mpmath(par):
 def _emulate_kernel(tab, z):
     """The kernel's interpolation (qm_rode.cuh) in numpy, to check the host table
     on CPU: segment select, quintic Hermite on (R, R', R''), log segment -> exp."""
-    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    H, SEG = 80, 32
+    NT, NC = int(tab[1]), int(tab[SEG + 4])                              # layout from the header
     out = np.empty(z.shape)
     for i, x in enumerate(z):
         side = 1 if x < 0 else 0
         a = abs(x)
         j = int(a >= tab[SEG + 24 * side + 8]) + int(a >= tab[SEG + 24 * side + 16])
-        w0, h, ih, k0, n, w1 = tab[SEG + 24 * side + 8 * j:SEG + 24 * side + 8 * j + 6]
-        s = min((a - w0) * ih, n)
+        w0, h, ih, k0, n, w1, G, g = tab[SEG + 24 * side + 8 * j:SEG + 24 * side + 8 * j + 8]
+        if g == 1:                       # octave levels: x = w/Wc = 2^e m, level l = e + 7, 512 intervals each
+            x = a * ih
+            m, e = np.frexp(x)           # x = m 2^e, m in [0.5, 1)
+            lv = min(max(int(e) - 1 + 7, 0), 6) if x > 0 else 0
+            u = (2 * m - 1) * 512.0                          # exact: 512 (mantissa - 1)
+            s = x * 32768.0 if lv == 0 else np.floor(u) + 512 * lv + (u - np.floor(u))  # t kept exact
+            h = w1 * 2.0 ** (max(lv, 1) - 16)
+        else:
+            s = (a - w0) * ih if g == 0 else n * (a * ih) ** (1.0 / g)  # graded: w = Wc (s/n)^g
+        s = min(s, n)
         fk = min(np.floor(s), n - 1)
         k, t = int(k0) + int(fk), s - fk
+        if g == 1 and lv > 0:
+            k, t = int(k0) + 512 * lv + int(np.floor(u)), u - np.floor(u)
         nd = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)
         (r0, d0, e0), (r1, d1, e1) = nd[k, :3], nd[k + 1, :3]
-        m0, m1, a0, a1, dp = h * d0, h * d1, h * h * e0, h * h * e1, r1 - r0
+        if g <= 1:
+            ws0 = ws1 = h
+            wss0 = wss1 = 0.0
+        else:                                                            # dw/ds, d2w/ds2 at the nodes
+            ws0, ws1 = g * G * fk ** (g - 1), g * G * (fk + 1) ** (g - 1)
+            wss0, wss1 = g * (g - 1) * G * fk ** (g - 2), g * (g - 1) * G * (fk + 1) ** (g - 2)
+        m0, m1, dp = ws0 * d0, ws1 * d1, r1 - r0
+        a0, a1 = ws0 * ws0 * e0 + wss0 * d0, ws1 * ws1 * e1 + wss1 * d1
         c3 = 10 * dp - 6 * m0 - 4 * m1 - 1.5 * a0 + 0.5 * a1
         c4 = -15 * dp + 8 * m0 + 7 * m1 + 1.5 * a0 - a1
         c5 = 6 * dp - 3 * m0 - 3 * m1 - 0.5 * a0 + 0.5 * a1
@@ -251,20 +285,22 @@ def test_product_student_table_vs_oracle(nu):
     """libqm's Student table (RODE backward from the far-tail anchor, in log t beyond
     |z| = 2; the centre forward from Q(0) = 0, Q'(0) = gamma): Q(0) and gamma come
     out as residuals, nodes of every segment equal the oracle's exact map, and the
-    kernel's interpolation (emulated) is within 4e-16 of it on |z| <= 6 -- the
-    paper's numerical solution promises 5e-8 there."""
+    kernel's interpolation (emulated) is within student_rode_bar of it (<= 1e-13 on
+    |z| <= 6; the paper's numerical solution promises 5e-8 there)."""
     from paper_0901_0638_b200.qm import STUDENT, qm_rode_table_host
     tab = qm_rode_table_host(STUDENT, [nu])
-    NT, H, SEG = 4096 + 16384 + 4096, 80, 32
+    H, SEG = 80, 32
+    NT, NC = int(tab[1]), int(tab[SEG + 4])                              # layout from the header
     assert tab[0] == 3 and tab[1] == NT and tab[31] == 1
     assert abs(tab[12]) < 1e-15 and abs(tab[14]) < 1e-15 and abs(tab[22]) < 1e-15
     nodes = tab[H:H + 4 * (NT + 1)].reshape(-1, 4)
     left = tab[H + 4 * (NT + 1):H + 8 * (NT + 1)].reshape(-1, 4)
-    for j, js in enumerate([[1, 37, 4000], [1, 5000, 16384], [0, 2000, 4094]]):
-        w0, h, ih, k0, n, w1 = tab[SEG + 8 * j:SEG + 8 * j + 6]
-        assert int(k0) == [0, 4096, 4096 + 16384 + 1][j] and abs(w0 + n * h - w1) <= 1e-15 * w1
+    for j, js in enumerate([[1, 37, 1800, 3200, 3400, 3584], [1, 5000, 16384], [0, 2000, 4094]]):
+        w0, h, ih, k0, n, w1, G, g = tab[SEG + 8 * j:SEG + 8 * j + 8]
+        assert int(k0) == [0, NC, NC + 16384 + 1][j] and abs(w0 + n * h - w1) <= 1e-15 * w1
+        assert g == (1 if j == 0 else 0)                                 # centre on octave levels
         js = np.array(js)
-        ex = O.student_exact(w0 + js * h, nu)
+        ex = O.student_exact(_node_w(tab, 0, j, js), nu)
         got = nodes[int(k0) + js, 0]
         if j == 2:
             assert np.max(np.abs(got / np.log(ex).astype(np.float64) - 1)) < 1e-15
@@ -278,9 +314,7 @@ def test_product_student_table_vs_oracle(nu):
     g = _emulate_kernel(tab, z)
     fin = np.isfinite(ex)
     rel = np.abs(g[fin] / ex[fin] - 1)
-    small = np.abs(z[fin]) <= 6
-    assert rel[small].max() < 4e-16 * 4
-    assert np.all(rel[~small] <= 2e-15 + 4 * 2.0 ** -52 * np.abs(np.log(np.abs(ex[fin][~small]))))
+    assert np.all(rel <= student_rode_bar(z[fin], ex[fin], nu))
 
 
 def test_product_student_table_rejects():
