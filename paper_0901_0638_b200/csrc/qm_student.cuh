@@ -21,7 +21,7 @@
 #include "qm_student_params.h"
 
 #ifndef QM_STUDENT_PAIR
-#define QM_STUDENT_PAIR 0   // A/B: 1 = the two samples of a double2 interleaved
+#define QM_STUDENT_PAIR 1   // 1 = the two samples of a double2 interleaved (+2-4 %); 0 = one by one; 2 = four
 #endif
 
 namespace qm {
@@ -186,7 +186,23 @@ struct MapStudentF64 {
     template <int PER>
     QM_DEV void map_slice(double2 *a) const
     {
-#if QM_STUDENT_PAIR
+#if QM_STUDENT_PAIR == 2
+        // four samples (two double2) interleaved: four independent DFMA chains
+        static_assert(PER % 2 == 0, "pairs of double2");
+#pragma unroll
+        for (int j = 0; j < PER; j += 2) {
+            const double c0 = student_central_k<K, KC>(*sp, fabs(a[j].x));
+            const double c1 = student_central_k<K, KC>(*sp, fabs(a[j].y));
+            const double c2 = student_central_k<K, KC>(*sp, fabs(a[j + 1].x));
+            const double c3 = student_central_k<K, KC>(*sp, fabs(a[j + 1].y));
+            const bool v0 = __any_sync(0xffffffffu, !(fabs(a[j].x) < sp->zstar));
+            const bool v1 = __any_sync(0xffffffffu, !(fabs(a[j].y) < sp->zstar));
+            const bool v2 = __any_sync(0xffffffffu, !(fabs(a[j + 1].x) < sp->zstar));
+            const bool v3 = __any_sync(0xffffffffu, !(fabs(a[j + 1].y) < sp->zstar));
+            a[j] = make_double2(student_finish(*sp, a[j].x, c0, v0), student_finish(*sp, a[j].y, c1, v1));
+            a[j + 1] = make_double2(student_finish(*sp, a[j + 1].x, c2, v2), student_finish(*sp, a[j + 1].y, c3, v3));
+        }
+#elif QM_STUDENT_PAIR
         // the two central series of a double2 in one basic block (two independent
         // DFMA chains), then the two votes and tails
 #pragma unroll
@@ -204,16 +220,19 @@ struct MapStudentF64 {
     }
 };
 
-// 1 CTA/SM: a producer warp + 16 consumer warps, 4 stages of 32 KB (2048 double2)
-// (A/B knobs: QM_STUDENT_NC consumer warps, QM_STUDENT_STAGES, QM_STUDENT_TV double2 per tile)
+// 1 CTA/SM: a producer warp + 16 consumer warps, 3 stages of 48 KB (3072 double2)
+// (A/B knobs: QM_STUDENT_NC consumer warps, QM_STUDENT_STAGES, QM_STUDENT_TV double2 per
+// tile; measured on one box, student nu = 4 / nu = 5 K = 16 Gsamples/s: 16 x 4 x 2048
+// one by one 267 / 250; pairs 275 / 256; pairs 16 x 3 x 3072 277 / 258; pairs 24 x 3 x
+// 3072 277 / 255; fours 274 / 256)
 #ifndef QM_STUDENT_NC
 #define QM_STUDENT_NC 16
 #endif
 #ifndef QM_STUDENT_STAGES
-#define QM_STUDENT_STAGES 4
+#define QM_STUDENT_STAGES 3
 #endif
 #ifndef QM_STUDENT_TV
-#define QM_STUDENT_TV 2048
+#define QM_STUDENT_TV 3072
 #endif
 constexpr int kStudentNC = QM_STUDENT_NC, kStudentStages = QM_STUDENT_STAGES, kStudentTileVecs = QM_STUDENT_TV;
 static_assert(kStudentTileVecs % (32 * kStudentNC) == 0, "a tile splits evenly over the consumer lanes");

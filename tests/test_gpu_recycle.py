@@ -35,7 +35,7 @@ def test_student_parity(nu, K, zstar, dtype, bar):
 
 @pytest.mark.parametrize("nu,K,zstar", STUDENT)
 def test_student_pipeline_equals_generic_kernel(nu, K, zstar):
-    """fp64, 16-byte aligned, K in {10, 16}: whole 4096-sample tiles run through the
+    """fp64, 16-byte aligned, K in {10, 16}: whole 6144-sample tiles run through the
     TMA pipeline with the series unrolled; a misaligned view runs the generic
     kernel.  Both must agree bitwise (specials placed inside the tiles)."""
     z = _z_inputs(np.float64)
