@@ -38,8 +38,10 @@ constexpr int kRodeTlStages = 3, kRodeTlTileVecs = 1024, kRodeTlNC = QM_RODE_TL_
 constexpr size_t kRodeTlTileBytes = (size_t)kRodeTlStages * kRodeTlTileVecs * 16;
 constexpr size_t kRodeTlSmemBytes = kRodeTlTileBytes + (size_t)(QM_RODE_HEADER + 2 * kRodeTlNodes * 3) * sizeof(double);
 
-// shared-memory layout: the table header (segment records, Vmax; 80 doubles)
-// then (R, R', R'') of nodes 0..M-1 of side 0, then of side 1
+// shared-memory layout: the table header (segment records, Vmax; 80 doubles),
+// then (R, R') pairs of nodes 0..M-1 of side 0 and of side 1 (16 B each: one
+// 128-bit load), then R'' of the same nodes (8 B each) -- 24 B per node, 4 loads
+// per sample (the two nodes of its interval) instead of 6
 constexpr int kRodeSmHdr = QM_RODE_HEADER;
 
 template <int M = kRodeSmemNodes>
@@ -49,8 +51,9 @@ QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
     for (int i = threadIdx.x; i < 2 * M; i += blockDim.x) {
         const int side = i / (M > 0 ? M : 1), k = i - side * M;
         const double *g = tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
-        double *d = sm + kRodeSmHdr + 3 * i;
-        d[0] = __ldg(g); d[1] = __ldg(g + 1); d[2] = __ldg(g + 2);
+        double *d = sm + kRodeSmHdr + 2 * i;
+        d[0] = __ldg(g); d[1] = __ldg(g + 1);
+        sm[kRodeSmHdr + 4 * M + i] = __ldg(g + 2);
     }
     __syncthreads();
 }
@@ -59,8 +62,9 @@ QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
 // gathers in flight together (a warp waits for its slowest lane: one lane with a
 // node in L2 stalls the warp for the L2 latency)
 struct RodePrep {
-    const double *b;     // node k of the sample's side (shared or global memory)
-    int st;              // doubles from node k to node k+1 (3 shared, 4 global)
+    const double *b;     // (R, R') of node k of the sample's side (shared or global memory)
+    const double *b2;    // R'' of node k
+    int st, st2;         // doubles from node k to node k+1 (shared 2 and 1, global 4 and 4)
     double t, a, vmax;
     // dw/ds and d2w/ds2 at nodes k and k+1 (s = the node coordinate): h and 0 on a
     // uniform segment; on the graded centre segment of a real-lambda VG table
@@ -163,8 +167,11 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     const int k = (int)r23.y + (int)fk;
     const bool in_sm = (M > 0) && (j == 0) && (k + 1 < M);
     RodePrep p;
-    p.b = in_sm ? sm + kRodeSmHdr + 3 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
-    p.st = in_sm ? 3 : 4;
+    // (R, R') of node k and its R'': shared (pairs array, R'' array) or global (4-double records)
+    p.b = in_sm ? sm + kRodeSmHdr + 2 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
+    p.b2 = in_sm ? sm + kRodeSmHdr + 4 * M + (side * M + k) : p.b + 2;
+    p.st = in_sm ? 2 : 4;
+    p.st2 = in_sm ? 1 : 4;
     p.t = t;
     p.a = a;
     p.vmax = side ? bd.vm1 : bd.vm0;
@@ -189,13 +196,14 @@ QM_DEV RodeNodes rode_load(const RodePrep &p)
         const double2 n1 = __ldg(reinterpret_cast<const double2 *>(p.b + 4));
         return RodeNodes{n0.x, n0.y, __ldg(p.b + 2), n1.x, n1.y, __ldg(p.b + 6)};
     } else {
-        return RodeNodes{p.b[0], p.b[1], p.b[2], p.b[p.st], p.b[p.st + 1], p.b[p.st + 2]};
+        return RodeNodes{p.b[0], p.b[1], p.b2[0], p.b[p.st], p.b[p.st + 1], p.b2[p.st2]};
     }
 }
 
 // quintic Hermite in monomial form: R(k h + t h) = p0 + m0 t + a0/2 t^2 + c3 t^3 + c4 t^4 + c5 t^5
+// (inside the table; rode_finish adds the extrapolation beyond Vmax)
 template <int MODE>
-QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
+QM_DEV double rode_interp(const RodePrep &p, const RodeNodes &n)
 {
     const double t = p.t;
     // derivatives with respect to s: dR/ds = R' w_s, d2R/ds2 = R'' w_s^2 + R' w_ss
@@ -207,7 +215,12 @@ QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
     const double c3 = 10.0 * dp - 6.0 * m0 - 4.0 * m1 - 1.5 * a0 + 0.5 * a1;
     const double c4 = -15.0 * dp + 8.0 * m0 + 7.0 * m1 + 1.5 * a0 - a1;
     const double c5 = 6.0 * dp - 3.0 * m0 - 3.0 * m1 - 0.5 * a0 + 0.5 * a1;
-    const double q = n.r0 + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
+    return n.r0 + t * (m0 + t * (0.5 * a0 + t * (c3 + t * (c4 + t * c5))));
+}
+template <int MODE>
+QM_DEV double rode_finish(const RodePrep &p, const RodeNodes &n)
+{
+    const double q = rode_interp<MODE>(p, n);
     const double qx = n.r1 + (p.a - p.vmax) * n.d1;             // beyond Vmax: node k+1 = node NT
     return (p.a <= p.vmax) ? q : qx;
 }
@@ -235,10 +248,16 @@ QM_DEV double rode_special(double v, double q)
 // node in shared memory: the coordinate of oct_coord, explicit shared loads, no
 // segment record.  Bitwise the same k, t and h as rode_prep.
 struct RodeFast {
-    uint32_t addr;       // shared address of node k's record
-    bool ok;             // a < Wc, node k+1 staged, finite
+    uint32_t addr, addr2;  // shared addresses of node k's (R, R') and R''
+    bool ok;               // a < Wc, node k+1 staged, finite
     RodePrep p;
 };
+QM_DEV double2 lds_f64x2(uint32_t addr)
+{
+    double2 r;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(addr));
+    return r;
+}
 template <int M>
 QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd)
 {
@@ -254,10 +273,13 @@ QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd
     f.p.wss0 = f.p.wss1 = 0.0;
     f.p.lg = false;
     f.p.neg = side != 0;
-    f.p.b = nullptr;
-    f.p.st = 3;
+    f.p.b = f.p.b2 = nullptr;
+    f.p.st = 2;
+    f.p.st2 = 1;
     f.ok = (a < wc) && (c.k + 1 < M);
-    f.addr = sm_nodes + 24u * (uint32_t)(side * M + min(c.k, M - 2));
+    const uint32_t node = (uint32_t)(side * M + min(c.k, M - 2));
+    f.addr = sm_nodes + 16u * node;
+    f.addr2 = sm_nodes + 32u * (uint32_t)M + 8u * node;
     return f;
 }
 
@@ -284,11 +306,12 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
             if (__all_sync(__activemask(), ok)) {
                 RodeNodes nd[G];
 #pragma unroll
-                for (int k = 0; k < G; ++k)
-                    nd[k] = RodeNodes{lds_f64(f[k].addr), lds_f64(f[k].addr + 8), lds_f64(f[k].addr + 16),
-                                      lds_f64(f[k].addr + 24), lds_f64(f[k].addr + 32), lds_f64(f[k].addr + 40)};
+                for (int k = 0; k < G; ++k) {
+                    const double2 n0 = lds_f64x2(f[k].addr), n1 = lds_f64x2(f[k].addr + 16);
+                    nd[k] = RodeNodes{n0.x, n0.y, lds_f64(f[k].addr2), n1.x, n1.y, lds_f64(f[k].addr2 + 8)};
+                }
 #pragma unroll
-                for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_finish<MODE>(f[k].p, nd[k]));
+                for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_interp<MODE>(f[k].p, nd[k]));
                 continue;
             }
         }

@@ -70,6 +70,13 @@ def make(name):
             fn = lambda: Q.qm_recycle_normal_to_t_rode(zn, tab, out=t)
         else:
             fn = lambda: Q.qm_recycle_normal_to_t(zn, 5.0, 16, out=t)
+    elif name == "rode_hyp_f64_ldg":       # misaligned view: the LDG kernel (no TMA input pipeline)
+        import numpy as np
+        from synth import inputs as I
+        tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+        v = torch.from_numpy(I.laplace(n + 1, dtype=np.float64)).cuda()[1:]
+        x = torch.empty(n + 1, dtype=torch.float64, device="cuda")[1:]
+        fn = lambda: Q.qm_recycle_exp_to_hyperbolic(v, tab, out=x)
     elif name in ("rode_hyp_f64", "rode_philox_f32"):
         import numpy as np
         from synth import inputs as I
