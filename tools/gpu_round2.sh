@@ -36,6 +36,8 @@ if [ "${PROFS:-all}" = all ]; then
   prof fused_f32_fma k_philox_f32 QM_LIB_PATH=paper_0901_0638_b200/ab/libqm_rat1.so fused_f32
   prof fused_f64 k_philox_f64
   prof student k_student_f64_tl
+  prof student_k16 k_student_f64_tl
+  prof student_rode k_rode_map_tl
   prof student_moments k_student_moments_tl
   prof moments k_moment_rows
   prof exp2n_f32 k_exp2n_f32_tl
@@ -50,6 +52,7 @@ if [ "${PROFS:-all}" = all ]; then
 fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file /tmp/launches.csv \
     python bench.py --steps 3 --warmup 3 --no-variants --no-cpu-baseline > $OUT/profiles/ncu_bench.log 2>&1
+timeout 300 python tools/window_curve.py stream_f32 10,20,50,100,200,400,1000 > $OUT/window_curve.jsonl 2>&1
 cp /tmp/launches.csv $OUT/profiles/launches_bench.csv
 python tools/ncu_summary.py --launches /tmp/launches.csv > $OUT/profiles/launches_bench_summary.json
 du -sh gpurun_out
