@@ -349,6 +349,9 @@ qm_status qm_normal_antithetic(const void *u, void *z, int64_t n, qm_precision p
     });
 }
 
+#ifndef QM_F64_FUSED_V
+#define QM_F64_FUSED_V 1   // A/B: Philox blocks (2 samples each) per lane per chunk of the fused fp64 sampler
+#endif
 static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_algorithm alg,
                                uint64_t seed, uint64_t c0, void *stream)
 {
@@ -372,7 +375,8 @@ static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_
     } else {
         const int g = grid_for((n + 1) / 2, kThreads, 8);
         if (mode == 0) k_philox_f64<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
-        else if (alg == QM_BREAKLESS) k_philox_f64<1, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+        else if (alg == QM_BREAKLESS)
+            k_philox_f64<1, ALG_BREAKLESS, QM_F64_FUSED_V><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
         else k_philox_f64<1, ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
     }
     return launched();

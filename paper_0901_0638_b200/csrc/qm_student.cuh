@@ -220,19 +220,20 @@ struct MapStudentF64 {
     }
 };
 
-// 1 CTA/SM: a producer warp + 16 consumer warps, 3 stages of 48 KB (3072 double2)
+// 1 CTA/SM: a producer warp + 16 consumer warps, 4 stages of 32 KB (2048 double2)
 // (A/B knobs: QM_STUDENT_NC consumer warps, QM_STUDENT_STAGES, QM_STUDENT_TV double2 per
-// tile; measured on one box, student nu = 4 / nu = 5 K = 16 Gsamples/s: 16 x 4 x 2048
-// one by one 267 / 250; pairs 275 / 256; pairs 16 x 3 x 3072 277 / 258; pairs 24 x 3 x
-// 3072 277 / 255; fours 274 / 256)
+// tile; measured on one box, nu = 4 K = 10 / nu = 5 K = 16 / nu = 3 K = 16 Gsamples/s:
+// one by one 268 / 244 / 228; pairs 275 / 251 / 235 (kept); pairs 3 x 3072 277 / 258 /
+// 181 -- a warp in the tail (13 % of a warp's tiles at nu = 3) holds a big stage
+// longer; pairs 6 x 2048 276 / 256 / 235; 8 x 1024 268 / 243 / 235; fours 274 / 251 / 231)
 #ifndef QM_STUDENT_NC
 #define QM_STUDENT_NC 16
 #endif
 #ifndef QM_STUDENT_STAGES
-#define QM_STUDENT_STAGES 3
+#define QM_STUDENT_STAGES 4
 #endif
 #ifndef QM_STUDENT_TV
-#define QM_STUDENT_TV 3072
+#define QM_STUDENT_TV 2048
 #endif
 constexpr int kStudentNC = QM_STUDENT_NC, kStudentStages = QM_STUDENT_STAGES, kStudentTileVecs = QM_STUDENT_TV;
 static_assert(kStudentTileVecs % (32 * kStudentNC) == 0, "a tile splits evenly over the consumer lanes");
