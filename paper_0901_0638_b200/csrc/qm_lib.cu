@@ -502,26 +502,30 @@ qm_status qm_exp_target_table(qm_target kind, const double *params, double *tabl
                ? QM_OK : QM_ECUDA;
 }
 
+// SIDES = 1: an odd map (the Student table, R35) -- one side's nodes staged, a larger ring
+extern "C++" {
+template <int SIDES>
 static qm_status rode_map_launch(const void *v, void *x, int64_t n, qm_precision p, const double *tab, void *stream)
 {
     if (n < 0 || bad_ptrs(v, x, n) || tab == nullptr || (p != QM_F32 && p != QM_F64)) return QM_EINVAL;
     if (n == 0) return QM_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    using C = RodeTl<SIDES>;
     // large aligned arrays: whole tiles through the TMA pipeline, the rest below
     int64_t done = 0;
     if (aligned16(v) && aligned16(x) && n >= ((int64_t)1 << 23)) {
-        const int64_t tile = (int64_t)kRodeTlTileVecs * (p == QM_F64 ? 2 : 4);
+        const int64_t tile = (int64_t)C::tile_vecs * (p == QM_F64 ? 2 : 4);
         const int64_t ntiles = n / tile;
         const int sms = sm_count_for_current_device();
         const int gg = (int)(ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148));
         auto tl = [&](auto k, auto *vv, auto *xx) {
-            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRodeTlSmemBytes) != cudaSuccess)
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes) != cudaSuccess)
                 return QM_ECUDA;
-            k<<<gg, 32 * (kRodeTlNC + 1), kRodeTlSmemBytes, s>>>(vv, xx, ntiles, tab);
+            k<<<gg, 32 * (kRodeTlNC + 1), C::smem_bytes, s>>>(vv, xx, ntiles, tab);
             return QM_OK;
         };
-        const qm_status r = (p == QM_F64) ? tl(k_rode_map_tl<double2>, (const double2 *)v, (double2 *)x)
-                                          : tl(k_rode_map_tl<float4>, (const float4 *)v, (float4 *)x);
+        const qm_status r = (p == QM_F64) ? tl(k_rode_map_tl<double2, SIDES>, (const double2 *)v, (double2 *)x)
+                                          : tl(k_rode_map_tl<float4, SIDES>, (const float4 *)v, (float4 *)x);
         if (r != QM_OK) return r;
         done = ntiles * tile;
         if (done == n) return launched();
@@ -530,28 +534,30 @@ static qm_status rode_map_launch(const void *v, void *x, int64_t n, qm_precision
         x = (char *)x + done * es;
         n -= done;
     }
-    // persistent: one 512-thread CTA per SM, each staging the centre nodes (197 KB)
+    // persistent: one 512-thread CTA per SM, each staging the centre nodes
     const int g = grid_for(n, 512 * 4, 1);
+    const size_t smem = rode_smem_bytes<SIDES>(kRodeSmemNodes);
     auto go = [&](auto k, auto *vv, auto *xx) {
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRodeSmemBytes) != cudaSuccess)
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return QM_ECUDA;
-        k<<<g, 512, kRodeSmemBytes, s>>>(vv, xx, n, tab);
+        k<<<g, 512, smem, s>>>(vv, xx, n, tab);
         return launched();
     };
-    if (p == QM_F64) return go(k_rode_map<double>, (const double *)v, (double *)x);
-    return go(k_rode_map<float>, (const float *)v, (float *)x);
+    if (p == QM_F64) return go(k_rode_map<double, SIDES>, (const double *)v, (double *)x);
+    return go(k_rode_map<float, SIDES>, (const float *)v, (float *)x);
 }
+}  // extern "C++"
 
 qm_status qm_recycle_exp_to_hyperbolic(const void *v, void *x, int64_t n, qm_precision p, const double *table_dev,
                                        void *stream)
 {
-    return rode_map_launch(v, x, n, p, table_dev, stream);
+    return rode_map_launch<2>(v, x, n, p, table_dev, stream);
 }
 
 qm_status qm_recycle_exp_to_vg(const void *v, void *x, int64_t n, qm_precision p, const double *table_dev,
                                void *stream)
 {
-    return rode_map_launch(v, x, n, p, table_dev, stream);
+    return rode_map_launch<2>(v, x, n, p, table_dev, stream);
 }
 
 qm_status qm_normal_target_table(qm_target kind, const double *params, double *table_dev)
@@ -567,7 +573,7 @@ qm_status qm_normal_target_table(qm_target kind, const double *params, double *t
 qm_status qm_recycle_normal_to_t_rode(const void *z, void *t, int64_t n, qm_precision p, const double *table_dev,
                                       void *stream)
 {
-    return rode_map_launch(z, t, n, p, table_dev, stream);
+    return rode_map_launch<1>(z, t, n, p, table_dev, stream);
 }
 
 qm_status qm_exp_base_quantile(const void *u, void *v, int64_t n, qm_precision p, const double *table_dev,

@@ -24,7 +24,10 @@ namespace qm {
 // Student table; rate |v| <= 2 = 86 % for a real-lambda VG table); the other
 // nodes are gathered from the table in global memory (L2-resident).
 constexpr int kRodeSmemNodes = QM_RODE_CENTRE_NODES + 1;
-constexpr size_t kRodeSmemBytes = (size_t)(QM_RODE_HEADER + 2 * kRodeSmemNodes * 3) * sizeof(double);
+// SIDES = 1: an odd map (Student, R35): only side 0 staged, the sign applied at the end
+template <int SIDES>
+constexpr size_t rode_smem_bytes(int m) { return (size_t)(QM_RODE_HEADER + SIDES * m * 3) * sizeof(double); }
+constexpr size_t kRodeSmemBytes = rode_smem_bytes<2>(kRodeSmemNodes);
 // with the TMA input pipeline (3 x 16 KB of stages) nodes 0..3599 of each side
 // (173 KB): every centre interval but the last
 #ifndef QM_RODE_TL_NODES
@@ -34,9 +37,23 @@ constexpr int kRodeTlNodes = QM_RODE_TL_NODES;
 #ifndef QM_RODE_TL_NC
 #define QM_RODE_TL_NC 16   // A/B knob: consumer warps of the RODE pipeline
 #endif
-constexpr int kRodeTlStages = 3, kRodeTlTileVecs = 1024, kRodeTlNC = QM_RODE_TL_NC;
-constexpr size_t kRodeTlTileBytes = (size_t)kRodeTlStages * kRodeTlTileVecs * 16;
-constexpr size_t kRodeTlSmemBytes = kRodeTlTileBytes + (size_t)(QM_RODE_HEADER + 2 * kRodeTlNodes * 3) * sizeof(double);
+constexpr int kRodeTlNC = QM_RODE_TL_NC;
+// the TMA ring: 3 x 16 KB beside both sides' nodes (173 KB); 4 x 32 KB beside one side's
+#ifndef QM_RODE_SYM_STAGES
+#define QM_RODE_SYM_STAGES 4
+#endif
+#ifndef QM_RODE_SYM_TILE
+#define QM_RODE_SYM_TILE 2048
+#endif
+template <int SIDES> struct RodeTl {
+    static constexpr int stages = SIDES == 2 ? 3 : QM_RODE_SYM_STAGES;
+    static constexpr int tile_vecs = SIDES == 2 ? 1024 : QM_RODE_SYM_TILE;
+    static constexpr size_t ring_bytes = (size_t)stages * tile_vecs * 16;
+    static constexpr size_t smem_bytes = ring_bytes + rode_smem_bytes<SIDES>(kRodeTlNodes);
+};
+static_assert(RodeTl<1>::smem_bytes <= 227 * 1024 && RodeTl<2>::smem_bytes <= 227 * 1024, "shared memory");
+constexpr int kRodeTlTileVecs = RodeTl<2>::tile_vecs;
+constexpr size_t kRodeTlSmemBytes = RodeTl<2>::smem_bytes;
 
 // shared-memory layout: the table header (segment records, Vmax; 80 doubles),
 // then (R, R') pairs of nodes 0..M-1 of side 0 and of side 1 (16 B each: one
@@ -44,16 +61,16 @@ constexpr size_t kRodeTlSmemBytes = kRodeTlTileBytes + (size_t)(QM_RODE_HEADER +
 // per sample (the two nodes of its interval) instead of 6
 constexpr int kRodeSmHdr = QM_RODE_HEADER;
 
-template <int M = kRodeSmemNodes>
+template <int M = kRodeSmemNodes, int SIDES = 2>
 QM_DEV void rode_stage_centre(const double *__restrict__ tab, double *sm)
 {
     for (int i = threadIdx.x; i < kRodeSmHdr; i += blockDim.x) sm[i] = __ldg(tab + i);
-    for (int i = threadIdx.x; i < 2 * M; i += blockDim.x) {
+    for (int i = threadIdx.x; i < SIDES * M; i += blockDim.x) {
         const int side = i / (M > 0 ? M : 1), k = i - side * M;
         const double *g = tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
         double *d = sm + kRodeSmHdr + 2 * i;
         d[0] = __ldg(g); d[1] = __ldg(g + 1);
-        sm[kRodeSmHdr + 4 * M + i] = __ldg(g + 2);
+        sm[kRodeSmHdr + 2 * SIDES * M + i] = __ldg(g + 2);
     }
     __syncthreads();
 }
@@ -140,10 +157,10 @@ QM_DEV OctCoord oct_coord(double x, double wc)
     return c;
 }
 
-template <int M, int MODE>
+template <int M, int MODE, int SIDES = 2>
 QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double *sm, const RodeBounds &bd)
 {
-    const int side = (v < 0.0) ? 1 : 0;
+    const int side = (SIDES == 2 && v < 0.0) ? 1 : 0;
     const double a = fabs(v);
     const double wc = side ? bd.wc1 : bd.wc0, vb = side ? bd.v1 : bd.v0;
     // segment j = [a >= Wc] + [a >= V] (selects; NaN lands in j = 0 and is replaced later)
@@ -169,7 +186,7 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     RodePrep p;
     // (R, R') of node k and its R'': shared (pairs array, R'' array) or global (4-double records)
     p.b = in_sm ? sm + kRodeSmHdr + 2 * (side * M + k) : tab + QM_RODE_HEADER + side * 4 * (QM_RODE_NT + 1) + 4 * k;
-    p.b2 = in_sm ? sm + kRodeSmHdr + 4 * M + (side * M + k) : p.b + 2;
+    p.b2 = in_sm ? sm + kRodeSmHdr + 2 * SIDES * M + (side * M + k) : p.b + 2;
     p.st = in_sm ? 2 : 4;
     p.st2 = in_sm ? 1 : 4;
     p.t = t;
@@ -258,10 +275,10 @@ QM_DEV double2 lds_f64x2(uint32_t addr)
     asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(addr));
     return r;
 }
-template <int M>
+template <int M, int SIDES = 2>
 QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd)
 {
-    const int side = (v < 0.0) ? 1 : 0;
+    const int side = (SIDES == 2 && v < 0.0) ? 1 : 0;
     const double a = fabs(v);
     const double wc = side ? bd.wc1 : bd.wc0, iwc = side ? bd.iwc1 : bd.iwc0;
     const OctCoord c = oct_coord(a * iwc, wc);
@@ -279,13 +296,16 @@ QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd
     f.ok = (a < wc) && (c.k + 1 < M);
     const uint32_t node = (uint32_t)(side * M + min(c.k, M - 2));
     f.addr = sm_nodes + 16u * node;
-    f.addr2 = sm_nodes + 32u * (uint32_t)M + 8u * node;
+    f.addr2 = sm_nodes + 16u * SIDES * (uint32_t)M + 8u * node;
     return f;
 }
 
 // B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
 // issued before their arithmetic (4 keeps the state in registers)
-template <int M, int MODE, int B>
+// SIDES = 1 (odd map): side 0 for |v|, the sign of v at the end
+QM_DEV double rode_odd(double v, double q) { return v < 0.0 ? -q : q; }
+
+template <int M, int MODE, int SIDES = 2, int B>
 QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const RodeBounds &bd, const double (&v)[B],
                            double (&x)[B])
 {
@@ -300,7 +320,7 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
             bool ok = true;
 #pragma unroll
             for (int k = 0; k < G; ++k) {
-                f[k] = rode_fast_prep<M>(v[g + k], smn, bd);
+                f[k] = rode_fast_prep<M, SIDES>(v[g + k], smn, bd);
                 ok = ok && f[k].ok;
             }
             if (__all_sync(__activemask(), ok)) {
@@ -311,18 +331,24 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
                     nd[k] = RodeNodes{n0.x, n0.y, lds_f64(f[k].addr2), n1.x, n1.y, lds_f64(f[k].addr2 + 8)};
                 }
 #pragma unroll
-                for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_interp<MODE>(f[k].p, nd[k]));
+                for (int k = 0; k < G; ++k) {
+                    const double q = rode_interp<MODE>(f[k].p, nd[k]);
+                    x[g + k] = rode_special(v[g + k], SIDES == 1 ? rode_odd(v[g + k], q) : q);
+                }
                 continue;
             }
         }
         RodePrep p[G];
         RodeNodes nd[G];
 #pragma unroll
-        for (int k = 0; k < G; ++k) p[k] = rode_prep<M, MODE>(tab, v[g + k], sm, bd);
+        for (int k = 0; k < G; ++k) p[k] = rode_prep<M, MODE, SIDES>(tab, v[g + k], sm, bd);
 #pragma unroll
         for (int k = 0; k < G; ++k) nd[k] = rode_load<M>(p[k]);
 #pragma unroll
-        for (int k = 0; k < G; ++k) x[g + k] = rode_special(v[g + k], rode_unlog<MODE>(p[k], rode_finish<MODE>(p[k], nd[k])));
+        for (int k = 0; k < G; ++k) {
+            const double q = rode_unlog<MODE>(p[k], rode_finish<MODE>(p[k], nd[k]));
+            x[g + k] = rode_special(v[g + k], SIDES == 1 ? rode_odd(v[g + k], q) : q);
+        }
     }
 }
 
@@ -335,7 +361,7 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
     default: CALL(kRodeGraded | kRodeOct | kRodeLog); break;                        \
     }
 
-template <typename T, int MODE>
+template <typename T, int MODE, int SIDES>
 QM_DEV void rode_map_body(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *__restrict__ tab,
                           const double *rode_sm, const RodeBounds &bd)
 {
@@ -345,21 +371,21 @@ QM_DEV void rode_map_body(const T *__restrict__ v, T *__restrict__ x, int64_t n,
         double a[U], r[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) a[k] = (i0 + k * S < n) ? (double)v[i0 + k * S] : 0.0;
-        rode_map_batch<kRodeSmemNodes, MODE>(tab, rode_sm, bd, a, r);
+        rode_map_batch<kRodeSmemNodes, MODE, SIDES>(tab, rode_sm, bd, a, r);
 #pragma unroll
         for (int k = 0; k < U; ++k)
             if (i0 + k * S < n) x[i0 + k * S] = (T)r[k];
     }
 }
 
-template <typename T>
+template <typename T, int SIDES = 2>
 __global__ void __launch_bounds__(512, 1)
 k_rode_map(const T *__restrict__ v, T *__restrict__ x, int64_t n, const double *__restrict__ tab)
 {
     extern __shared__ __align__(16) double rode_sm[];
-    rode_stage_centre(tab, rode_sm);
+    rode_stage_centre<kRodeSmemNodes, SIDES>(tab, rode_sm);
     const RodeBounds bd = rode_bounds(tab);
-#define QM_RODE_MAP_CALL(MD) rode_map_body<T, MD>(v, x, n, tab, rode_sm, bd)
+#define QM_RODE_MAP_CALL(MD) rode_map_body<T, MD, SIDES>(v, x, n, tab, rode_sm, bd)
     QM_RODE_DISPATCH(tab, QM_RODE_MAP_CALL)
 #undef QM_RODE_MAP_CALL
 }
@@ -371,7 +397,7 @@ template <typename V> struct RodeVec;
 template <> struct RodeVec<double2> { using T = double; static constexpr int W = 2; };
 template <> struct RodeVec<float4> { using T = float; static constexpr int W = 4; };
 
-template <typename V, int MODE>
+template <typename V, int MODE, int SIDES>
 struct MapRode {
     const double *tab;
     const double *sm;
@@ -385,22 +411,23 @@ struct MapRode {
         double in[PER * W], out[PER * W];
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) in[k] = (double)e[k];
-        rode_map_batch<kRodeTlNodes, MODE>(tab, sm, bd, in, out);
+        rode_map_batch<kRodeTlNodes, MODE, SIDES>(tab, sm, bd, in, out);
 #pragma unroll
         for (int k = 0; k < PER * W; ++k) e[k] = (T)out[k];
     }
 };
 
-template <typename V>
+template <typename V, int SIDES = 2>
 __global__ void __launch_bounds__(32 * (kRodeTlNC + 1), 1)
 k_rode_map_tl(const V *__restrict__ v, V *__restrict__ x, int64_t ntiles, const double *__restrict__ tab)
 {
+    using C = RodeTl<SIDES>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double *sm = reinterpret_cast<double *>(smem_raw + kRodeTlTileBytes);
-    rode_stage_centre<kRodeTlNodes>(tab, sm);
+    double *sm = reinterpret_cast<double *>(smem_raw + C::ring_bytes);
+    rode_stage_centre<kRodeTlNodes, SIDES>(tab, sm);
     const RodeBounds bd = rode_bounds(tab);
 #define QM_RODE_TL_CALL(MD) \
-    tma_load_map<V, kRodeTlTileVecs, kRodeTlStages, kRodeTlNC>(v, x, ntiles, MapRode<V, MD>{tab, sm, bd})
+    tma_load_map<V, C::tile_vecs, C::stages, kRodeTlNC>(v, x, ntiles, MapRode<V, MD, SIDES>{tab, sm, bd})
     QM_RODE_DISPATCH(tab, QM_RODE_TL_CALL)
 #undef QM_RODE_TL_CALL
 }
@@ -454,7 +481,7 @@ QM_DEV void rode_philox_body(T *__restrict__ x, int64_t n, unsigned long long se
         }
 #pragma unroll
         for (int k = 0; k < 2 * W; ++k) u[k] = exp_base_quantile(tab, u[k]);
-        rode_map_batch<kRodeSmemNodes, MODE>(tab, rode_sm, bd, u, r);
+        rode_map_batch<kRodeSmemNodes, MODE, 2>(tab, rode_sm, bd, u, r);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t b = b0 + h * stride;
