@@ -589,9 +589,10 @@ def run_ours(args):
     z = torch.empty_like(u)
     step = lambda: Q.qm_normal_quantile(u, out=z)
 
-    # a rested GPU (R34, tools/window_curve.py): the 1000 W controller steps the SM clock
-    # down after ~45-60 ms of this load, so the default K = 100 launches (~40 ms) measure
-    # the unthrottled rate; `sustained` below is the power-capped one
+    # a rested GPU (R34, tools/window_curve.py): after the rest the first ~10-15 launches
+    # ramp up and the 1000 W controller steps the SM clock down after ~100-110 launches
+    # (~45 ms), so the defaults W = 20, K = 80 time launches 21-100, the unthrottled
+    # rate; `sustained` below is the power-capped one
     torch.cuda.synchronize()
     time.sleep(1.0)
     sampler = ClockSampler(local)
@@ -691,8 +692,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=80)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
