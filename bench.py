@@ -57,56 +57,82 @@ def load_traffic():
     return {}
 
 
+_POLLER = r"""
+import json, sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+    getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+print("ready", flush=True)
+import select
+ts, sm, pw, rs = [], [], [], []
+while not select.select([sys.stdin], [], [], 0)[0]:
+    try:
+        t = time.perf_counter()
+        c = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        r = int(get_reasons(h))
+        w = pynvml.nvmlDeviceGetPowerUsage(h) / 1e3
+        ts.append(t); sm.append(c); rs.append(r); pw.append(w)
+    except Exception:
+        pass
+    time.sleep(0.001)
+print(json.dumps({"t": ts, "sm": sm, "pw": pw, "rs": rs, "max": mx}), flush=True)
+"""
+
+
 class ClockSampler:
-    """Polls NVML (SM clock, clock-event reasons) every ~2 ms during a timed region."""
+    """Polls NVML (SM clock, clock-event reasons, power) every ~1 ms during a timed
+    region, in a separate process (a thread in this one shares the GIL with the
+    launch loop and samples only a few times)."""
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
                0x2: "applications_clocks_setting", 0x10: "sync_boost"}
 
     def __init__(self, index):
+        self.index = index
         self.ok = False
+        self.max_mhz = None
+        self.t, self.samples, self.reasons, self.power = [], [], [], []
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            import pynvml  # noqa: F401
             self.ok = True
         except Exception:
-            self.max_mhz = None
-        self.samples, self.reasons, self.power = [], 0, []
-        self._stop = threading.Event()
-
-    def _run(self):
-        nv = self.nv
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                self.reasons |= int(get_reasons(self.h))
-                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
-            except Exception:
-                pass
-            time.sleep(0.002)
+            pass
 
     def __enter__(self):
         if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+            import subprocess
+            self.p = subprocess.Popen([sys.executable, "-c", _POLLER, str(self.index)], stdin=subprocess.PIPE,
+                                      stdout=subprocess.PIPE, text=True)
+            if self.p.stdout.readline().strip() != "ready":
+                self.ok = False
         return self
 
     def __exit__(self, *a):
         if self.ok:
-            self._stop.set()
-            self.t.join()
+            out, _ = self.p.communicate("stop\n", timeout=60)
+            try:
+                d = json.loads(out.strip().splitlines()[-1])
+                self.t, self.samples, self.power, self.reasons = d["t"], d["sm"], d["pw"], d["rs"]
+                self.max_mhz = d["max"]
+            except Exception:
+                self.ok = False
 
-    def summary(self):
-        if not self.ok or not self.samples:
+    def summary(self, t0=None, t1=None):
+        """over the whole region, or over the samples taken in [t0, t1] (time.perf_counter)"""
+        idx = [i for i, t in enumerate(self.t) if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
+        if not self.ok or not idx:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1),
-                "n_samples": len(self.samples), "power_w_max": max(self.power) if self.power else None}
+        sm = [self.samples[i] for i in idx]
+        pw = [self.power[i] for i in idx]
+        rs = 0
+        for i in idx:
+            rs |= self.reasons[i]
+        return {"sm_mhz": float(statistics.median(sm)), "sm_max_mhz": self.max_mhz, "sm_mhz_min": float(min(sm)),
+                "reasons": sorted(v for k, v in self.REASONS.items() if rs & k and k != 0x1),
+                "n_samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
 def dist_setup(gpus):
@@ -454,16 +480,19 @@ def sustained_rate(fn, n, bytes_per, windows=12, launches=250, keep=8, index=0):
     import torch
     rows = []
     s = torch.cuda.current_stream()
-    for _ in range(windows):
-        with ClockSampler(index) as cs:
+    spans = []
+    with ClockSampler(index) as cs:
+        for _ in range(windows):
+            t0 = time.perf_counter()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             for _ in range(launches):
                 fn()
             e1.record(s)
             torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / launches
-        c = cs.summary()
+            spans.append((t0, time.perf_counter(), e0.elapsed_time(e1) / launches))
+    for t0, t1, ms in spans:
+        c = cs.summary(t0, t1)
         rows.append((n / (ms / 1e3) / 1e9, c.get("sm_mhz"), c.get("power_w_max"), c.get("reasons")))
     tail = rows[-keep:]
     g = statistics.median(r[0] for r in tail)
