@@ -20,6 +20,14 @@
 
 #include "qm_student_params.h"
 
+#ifndef QM_STUDENT_DEFER
+// A/B: 1 = one vote per slice and the lane's tails one at a time (below).  Measured
+// (same box, Gsamples/s, defer / per-position votes): nu = 3 241 / 237, nu = 4 274 /
+// 276, nu = 5 254 / 253, nu = 10 253 / 257, fused moments 234 / 238 -- the tail is
+// not what separates nu = 3 from nu = 5 (a caller z* beyond every sample runs nu = 3
+// at 250), so the simpler per-position vote stays
+#define QM_STUDENT_DEFER 0
+#endif
 #ifndef QM_STUDENT_PAIR
 #define QM_STUDENT_PAIR 1   // 1 = the two samples of a double2 interleaved (+2-4 %); 0 = one by one; 2 = four
 #endif
@@ -186,7 +194,44 @@ struct MapStudentF64 {
     template <int PER>
     QM_DEV void map_slice(double2 *a) const
     {
-#if QM_STUDENT_PAIR == 2
+#if QM_STUDENT_DEFER
+        // The central series of the lane's 2 PER samples (two chains at a time), then
+        // the tails: each lane keeps a bit mask of its samples with |z| >= z* (or NaN)
+        // and, while any lane of the warp has one left, every lane evaluates the tail
+        // for its next one.  One vote per slice (2 PER x 32 samples) instead of one per
+        // element position: at nu = 3 a warp meets a tail in 8.8 % of its slices and
+        // then pays one tail evaluation, not one per position that has a tail lane.
+        // Bitwise the same values as student_map (the tail at max(|z|, z*)).
+        constexpr int NS = 2 * PER;
+        double z[NS], t[NS];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            z[2 * j] = a[j].x;
+            z[2 * j + 1] = a[j].y;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            t[2 * j] = student_central_k<K, KC>(*sp, fabs(z[2 * j]));
+            t[2 * j + 1] = student_central_k<K, KC>(*sp, fabs(z[2 * j + 1]));
+        }
+        uint32_t need = 0;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) need |= (uint32_t)(!(fabs(z[k]) < sp->zstar)) << k;
+        while (__any_sync(0xffffffffu, need != 0)) {
+            const int kk = __ffs(need) - 1;                          // -1: this lane has none left
+            double zs = 0.0;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) zs = (kk == k) ? z[k] : zs;
+            const double tt = student_tail(*sp, fmax(fabs(zs), sp->zstar));
+#pragma unroll
+            for (int k = 0; k < NS; ++k) t[k] = (kk == k && fabs(z[k]) >= sp->zstar) ? tt : t[k];
+            need &= need - 1;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) t[k] = student_finish(*sp, z[k], t[k], false);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) a[j] = make_double2(t[2 * j], t[2 * j + 1]);
+#elif QM_STUDENT_PAIR == 2
         // four samples (two double2) interleaved: four independent DFMA chains
         static_assert(PER % 2 == 0, "pairs of double2");
 #pragma unroll

@@ -62,11 +62,12 @@ def make(name):
         zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
         t = torch.empty_like(zn)
         fn = lambda: Q.qm_recycle_normal_to_t(zn, 4.0, 10, 3.93473, out=t)
-    elif name in ("student_nu3", "student_nu10"):
+    elif name in ("student_nu3", "student_nu10", "student_nu3_notail"):
         zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
         t = torch.empty_like(zn)
-        nu = 3.0 if name == "student_nu3" else 10.0
-        fn = lambda: Q.qm_recycle_normal_to_t(zn, nu, 16, out=t)
+        nu = 10.0 if name == "student_nu10" else 3.0
+        zs = 50.0 if name == "student_nu3_notail" else 0.0     # A/B: the series alone (caller z* beyond every sample)
+        fn = lambda: Q.qm_recycle_normal_to_t(zn, nu, 16, zs, out=t)
     elif name in ("student_rode", "student_k16"):
         zn = Q.qm_normal_philox(1 << 30, SEED, 0, dtype=torch.float64)
         t = torch.empty_like(zn)
@@ -101,7 +102,7 @@ def make(name):
 def _count(name, n):
     big = {"fused_f32": 1 << 32, "fused_f64": 1 << 31, "moments": 1 << 30, "mc": 1 << 32, "student_moments": 1 << 30,
            "student": 1 << 30, "student_rode": 1 << 30, "student_k16": 1 << 30, "student_nu3": 1 << 30,
-           "student_nu10": 1 << 30}
+           "student_nu10": 1 << 30, "student_nu3_notail": 1 << 30}
     if name.startswith("config1_") or name.startswith("plain_config1_"):
         return 1 << 20
     return big.get(name, n)
