@@ -29,6 +29,7 @@ template <int ALG>
 __global__ void __launch_bounds__(kThreads, 4)
 k_normal_f32(const float *__restrict__ u, float *__restrict__ z, int64_t n, int vec)
 {
+    pdl_begin();                                          // launched with PDL (qm_lib.cu)
     constexpr int V = 2;                                  // float4 per lane per chunk
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -590,6 +591,7 @@ template <int ALG>
 __global__ void __launch_bounds__(kThreads)
 k_exp2n_f32(const float *__restrict__ v, float *__restrict__ z, int64_t n, int vec)
 {
+    pdl_begin();                                          // launched with PDL (qm_lib.cu)
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;

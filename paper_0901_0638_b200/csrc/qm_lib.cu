@@ -92,6 +92,35 @@ bool tma_enabled() { return stream_path() != 0; }
 
 // fp32 elementwise map: whole tiles through the TMA pipeline (persistent CTAs),
 // the remainder (< 1 tile) and misaligned arrays through the LDG kernel.
+// Programmatic dependent launch: the kernel may start while the previous grid on
+// the stream drains (its prologue overlaps that grid's tail and the launch gap);
+// it waits in pdl_begin() (qm_tma.cuh) before touching global memory.  QM_PDL=0
+// launches normally (A/B).
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = getenv("QM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename K, typename... Args>
+void launch_pdl(K kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 template <class CFG, typename KT, typename KL>
 qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64_t n, cudaStream_t s)
 {
@@ -106,12 +135,12 @@ qm_status launch_stream_f32(KT ktma, KL kldg, const float *in, float *out, int64
         const int sms = sm_count_for_current_device();
         int64_t g = (int64_t)(sms > 0 ? sms : 148) * CFG::MINB;
         if (ntiles < g) g = ntiles;
-        ktma<<<(int)g, CFG::THREADS, smem, s>>>(in, out, ntiles);
+        launch_pdl(ktma, (unsigned)g, CFG::THREADS, smem, s, in, out, ntiles);
     }
     const int64_t done = ntiles * CFG::TILE, rest = n - done;
     if (rest > 0) {
         const int g = grid_for(rest, kThreads * 8, 8);
-        kldg<<<g, kThreads, 0, s>>>(in + done, out + done, rest, vec);
+        launch_pdl(kldg, (unsigned)g, kThreads, 0, s, in + done, out + done, rest, vec);
     }
     return launched();
 }

@@ -26,6 +26,17 @@
 
 namespace qm {
 
+// Programmatic dependent launch (the streaming maps are launched with it, qm_lib.cu):
+// let the next grid on the stream launch now (its CTAs take SMs as ours exit and
+// wait below), and wait for every prior grid to complete -- with its memory
+// visible -- before this grid's first global access.  No-ops for a normal launch.
+__device__ __forceinline__ void pdl_begin()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+
 QM_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 QM_DEV void mbar_init(uint64_t *bar, uint32_t count)
@@ -105,6 +116,7 @@ __device__ __forceinline__ void tma_stream_map(const T *__restrict__ in, T *__re
         for (int s = 0; s < STAGES; ++s) { mbar_init_elect(&full[s], 1); mbar_init_elect(&empty[s], 1); }
         fence_mbar_init();
     }
+    pdl_begin();
     __syncthreads();
 
     const int64_t first = blockIdx.x, step = gridDim.x;
@@ -182,6 +194,7 @@ __device__ __forceinline__ void tma_load_map(const V *__restrict__ in, V *__rest
         for (int s = 0; s < STAGES; ++s) { mbar_init_elect(&full[s], 1); mbar_init_elect(&empty[s], NC); }
         fence_mbar_init();
     }
+    pdl_begin();
     __syncthreads();
 
     const int64_t first = blockIdx.x, step = gridDim.x;
