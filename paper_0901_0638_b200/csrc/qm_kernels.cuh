@@ -366,6 +366,7 @@ template <int MODE, int ALG, int V = 2, int MINB = 1>   // V: Philox blocks per 
 __global__ void __launch_bounds__(kThreads, MINB)
 k_philox_f32(float *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
 {
+    pdl_begin();                                          // launched with PDL (qm_lib.cu)
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -427,6 +428,7 @@ template <int MODE, int ALG, int V = 1>   // V Philox blocks (2V samples) per la
 __global__ void __launch_bounds__(kThreads)
 k_philox_f64(double *__restrict__ z, int64_t n, unsigned long long seed, unsigned long long c0, int vec)
 {
+    pdl_begin();                                          // launched with PDL (qm_lib.cu)
     const PhiloxKeys keys(seed);
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

@@ -393,20 +393,20 @@ static qm_status philox_launch(void *z, int64_t n, qm_precision p, int mode, qm_
         const int64_t nb = (n + 3) / 4;
         if (mode == 0) {
             auto k = k_philox_f32<0, ALG_BREAKLESS>;
-            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+            launch_pdl(k, grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s, (float *)z, n, seed, c0, vec);
         } else if (alg == QM_BREAKLESS) {
             auto k = k_philox_f32<1, ALG_BREAKLESS>;
-            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+            launch_pdl(k, grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s, (float *)z, n, seed, c0, vec);
         } else {
             auto k = k_philox_f32<1, ALG_BREAKLESS77>;
-            k<<<grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s>>>((float *)z, n, seed, c0, vec);
+            launch_pdl(k, grid_resident(k, kThreads, nb, kThreads * 2), kThreads, 0, s, (float *)z, n, seed, c0, vec);
         }
     } else {
         const int g = grid_for((n + 1) / 2, kThreads, 8);
-        if (mode == 0) k_philox_f64<0, ALG_BREAKLESS><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+        if (mode == 0) launch_pdl(k_philox_f64<0, ALG_BREAKLESS>, g, kThreads, 0, s, (double *)z, n, seed, c0, vec);
         else if (alg == QM_BREAKLESS)
-            k_philox_f64<1, ALG_BREAKLESS, QM_F64_FUSED_V><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
-        else k_philox_f64<1, ALG_BREAKLESS77><<<g, kThreads, 0, s>>>((double *)z, n, seed, c0, vec);
+            launch_pdl(k_philox_f64<1, ALG_BREAKLESS, QM_F64_FUSED_V>, g, kThreads, 0, s, (double *)z, n, seed, c0, vec);
+        else launch_pdl(k_philox_f64<1, ALG_BREAKLESS77>, g, kThreads, 0, s, (double *)z, n, seed, c0, vec);
     }
     return launched();
 }
