@@ -507,8 +507,8 @@ def sustained_rate(fn, n, bytes_per, windows=12, launches=250, keep=8, index=0):
 
 def size_sweep(Q, torch, peaks):
     """Gsamples/s and roofline fraction over 2^20 .. 2^34 samples (north star), 1 GPU:
-    the fp32 streaming map (inputs resident in HBM; in place from 2^33, where in +
-    out would not leave room) and the Philox-fused fp32 sampler.  Sizes whose launch
+    the fp32 streaming map (inputs resident in HBM, out of place) and the
+    Philox-fused fp32 sampler.  Sizes whose launch
     is shorter than ~1 ms are timed as CUDA graphs of 50 launches.  Each entry is a
     burst (as the headline: a few warm-up launches, then the timed ones); from 2^28
     on the sustained (power-settled) rate is given too."""
@@ -542,9 +542,17 @@ def size_sweep(Q, torch, peaks):
 
     for e in range(20, 35):
         n = 1 << e
-        u = torch.empty(n, dtype=torch.float32, device="cuda")
+        # out of place at every size (2^34: 2 x 64 GiB): repeated in-place launches would
+        # map their own outputs -- normals, not uniforms -- through the careful path
+        try:
+            u = torch.empty(n, dtype=torch.float32, device="cuda")
+            z = torch.empty_like(u)
+        except torch.cuda.OutOfMemoryError:
+            res["stream_f32"][f"2^{e}"] = {"skipped": "input + output do not fit beside the other allocations"}
+            u = z = None
+            torch.cuda.empty_cache()
+            continue
         Q.qm_philox_uniform(n, SEED, 0, out=u)
-        z = u if e >= 33 else torch.empty_like(u)
         timed(lambda: Q.qm_normal_quantile(u, out=z), n, "stream_f32", 8, sustained=e >= 28 and e % 2 == 0)
         del u, z
         torch.cuda.empty_cache()
@@ -554,7 +562,7 @@ def size_sweep(Q, torch, peaks):
         timed(lambda: Q.qm_normal_philox(n, SEED, 0, out=z), n, "fused_f32", 4)
         del z
         torch.cuda.empty_cache()
-    res["note"] = ("stream_f32 from 2^33 maps in place (2^34 fp32 = 64 GiB); hbm_frac of the fused sampler is its "
+    res["note"] = ("stream_f32 out of place at every size (2^34: 2 x 64 GiB); hbm_frac of the fused sampler is its "
                    "write-only 4 B/sample against the copy bandwidth, not its bound (issue / FP64 pipe)")
     return res
 

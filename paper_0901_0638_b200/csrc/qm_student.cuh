@@ -96,7 +96,14 @@ QM_DEV double exp_plain(double x)
     return t * s1 * s2;
 }
 
+#ifndef QM_STUDENT_TAIL_NOINLINE
+#define QM_STUDENT_TAIL_NOINLINE 1   // the rarely taken tail out of line: a compact hot loop (A/B same box: nu = 3 240 -> 246, nu = 4 276 -> 281, nu = 5 260 -> 260)
+#endif
+#if QM_STUDENT_TAIL_NOINLINE
+__device__ __noinline__ double student_tail(const StudentParams &sp, double a)
+#else
 QM_DEV double student_tail(const StudentParams &sp, double a)
+#endif
 {
     // log w = log(erfc(a/sqrt2)) + log(C_nu/2); erfc(x) = exp(-x^2) erfcx(x)
     const double xh = __dmul_rn(a, 0.70710678118654752440);
