@@ -1,16 +1,18 @@
-// qm_rode.cuh -- exponential-base recycling into hyperbolic / variance-gamma
-// samples (§4 of the paper).
+// qm_rode.cuh -- recycling by a numerically solved Recycling ODE: exponential
+// base into hyperbolic / variance-gamma samples (§4 of the
+// paper) and Gaussian base into Student-t samples (§3.6, P:282-283;
+// reading R35).
 //
-// The map Q(v) is the numerically solved Recycling ODE (built on the host by
-// qm_rode_host.cpp into a table of (Q, Q', Q'') at the nodes of a centre, a fine
-// (out to base probability e^-40) and a coarse segment (out to e^-800), per
-// side; see qm_rode_params.h).  Per sample the kernel does a quintic Hermite interpolation
-// between two nodes (four 16-byte gathers from the table, which stays in L2/L1;
-// the error is O(h^6), needed for relative accuracy near v = 0).  Past e^-800
-// (no double uniform reaches it) linear extrapolation with the end slope
-// (Q' -> 1 in the tails).  Side and segment are selects, not branches.
-// The fused sampler draws u from Philox and applies the base quantile Q0 of
-// P:322-329 first.
+// The map Q(v) is built on the host (qm_rode_host.cpp) into a table of (Q, Q', Q'')
+// at the nodes of a centre (octave levels, R36), a fine and a coarse segment per
+// side (qm_rode_params.h).  Per sample the kernel does a quintic Hermite
+// interpolation between two nodes (the error is O(h^6), relative accuracy near
+// v = 0 from the octave spacing); the centre's nodes are staged in shared memory
+// and a warp whose samples all lie there takes a fast path (explicit shared
+// loads, the coordinate from the bits of |v|/Wc).  Past the last node (no double
+// uniform reaches it) linear extrapolation with the end slope (Q' -> 1 in the
+// tails; log-linear for the Student table).  The fused sampler draws u
+// from Philox and applies the base quantile Q0 of P:322-329 first.
 #pragma once
 #include "qm_dd.cuh"
 #include "qm_rode_params.h"
@@ -19,7 +21,7 @@
 namespace qm {
 
 // Centre-segment nodes staged in shared memory: (R, R', R'') per node, 3 doubles,
-// nodes 0..Nc of both sides (2 x 3601 x 24 B = 173 KB).  The centre covers
+// nodes 0..Nc of both sides (2 x 3585 x 24 B = 172 KB).  The centre covers
 // rate |v| <= 10 (99.995 % of the base samples; |z| <= 4.5 = 1 - 7e-6 for the
 // Student table; rate |v| <= 2 = 86 % for a real-lambda VG table); the other
 // nodes are gathered from the table in global memory (L2-resident).
@@ -28,8 +30,8 @@ constexpr int kRodeSmemNodes = QM_RODE_CENTRE_NODES + 1;
 template <int SIDES>
 constexpr size_t rode_smem_bytes(int m) { return (size_t)(QM_RODE_HEADER + SIDES * m * 3) * sizeof(double); }
 constexpr size_t kRodeSmemBytes = rode_smem_bytes<2>(kRodeSmemNodes);
-// with the TMA input pipeline (3 x 16 KB of stages) nodes 0..3599 of each side
-// (173 KB): every centre interval but the last
+// with the TMA input pipeline nodes 0..Nc-1 of each side: every centre interval
+// but the last
 #ifndef QM_RODE_TL_NODES
 #define QM_RODE_TL_NODES QM_RODE_CENTRE_NODES
 #endif
