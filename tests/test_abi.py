@@ -72,6 +72,18 @@ def test_argument_validation_before_launch(lib):
     assert lib.qm_philox_uniform(None, 3, L.QM_F32, 1, 0, None) == L.QM_EINVAL
     assert lib.qm_normal_quantile_host(p, p, -3, L.QM_F32, 0) == L.QM_EINVAL
     assert lib.qm_status_string(L.QM_EUNSUPPORTED).decode() == "unsupported combination"
+    # §3.6 Student table (R35): kind, nu range -- all decided before any CUDA call
+    nu = (ctypes.c_double * 3)
+    assert lib.qm_normal_target_table(L.QM_TARGET_HYPERBOLIC, nu(4.0), p) == L.QM_EINVAL
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, None, p) == L.QM_EINVAL
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, nu(4.0), None) == L.QM_EINVAL
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, nu(0.0), p) == L.QM_EINVAL
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, nu(float("nan")), p) == L.QM_EINVAL
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, nu(0.5), p) == L.QM_EUNSUPPORTED
+    assert lib.qm_normal_target_table(L.QM_TARGET_STUDENT, nu(201.0), p) == L.QM_EUNSUPPORTED
+    assert lib.qm_recycle_normal_to_t_rode(p, p, 4, L.QM_F64, None, None) == L.QM_EINVAL
+    assert lib.qm_recycle_normal_to_t_rode(p, p, 4, 3, p, None) == L.QM_EINVAL
+    assert lib.qm_recycle_normal_to_t_rode(p, p, 0, L.QM_F64, p, None) == L.QM_OK
 
 
 @pytest.mark.parametrize("nu,K", [(4.0, 10), (3.0, 16), (5.0, 16), (10.0, 16), (10.0, 24), (20.0, 16), (1.0, 12)])
