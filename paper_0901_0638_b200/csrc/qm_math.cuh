@@ -399,7 +399,8 @@ QM_DEV dd two_sum_ord(double p, double a)
     return dd{t, __dadd_rn(lo, -__dadd_rn(t, -hi))};
 }
 
-template <int N, int KC>
+// ZL = false: P(zh) only -- z's low part is left to the caller (rational_dd)
+template <int N, int KC, bool ZL = true>
 QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 {
     double s = a[N - 1], c = 0.0;
@@ -411,7 +412,8 @@ QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
             const double p = __dmul_rn(s, zh);
             const double pi = __fma_rn(s, zh, -p);               // TwoProd
             const dd t = two_sum_pos(p, a[i]);                   // Fast2Sum, ordered
-            c = __fma_rn(c, zh, __fma_rn(s, zl, __dadd_rn(pi, t.lo)));
+            const double err = __dadd_rn(pi, t.lo);
+            c = __fma_rn(c, zh, ZL ? __fma_rn(s, zl, err) : err);
             s = t.hi;
         }
     }
@@ -419,12 +421,23 @@ QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 }
 
 // z P(z)/Q(z) for a double-double z >= 0, one final rounding (positive
-// coefficients: the breakless rationals)
+// coefficients: the breakless rationals).
+// z's low part zl (|zl| <= 2^-53 zh) enters once, as zl R(zh) in the final sum,
+// not in every compensated Horner step (QM_DD_ZL_STEPS=1 restores the per-step
+// form): (zh + zl) R(zh + zl) = zh R + zl R + zh zl R' + O(zl^2), and the dropped
+// zh zl R' is (zl/zh)(kappa - 1) of the result, kappa = d ln(zR)/d ln z.  On the
+// fp64 grid (z <= 36.04) |kappa - 1| <= 0.473 for App D, so this adds <= 0.473 ulp:
+// with the plain steps' W_P + W_Q it stays <= 1.04 + 0.5 (final rounding) ulp
+// (tests/test_oracle_normal.py::test_d13_partial_compensation_bound), and it saves
+// one DFMA per compensated step (20 of App D's ~211 FP64 operations per sample).
+#ifndef QM_DD_ZL_STEPS
+#define QM_DD_ZL_STEPS 0
+#endif
 template <int N, int KC>
 QM_DEV double rational_dd(dd z, const double *P, const double *Q)
 {
-    const dd p = horner_comp_pos<N, KC>(P, z.hi, z.lo);
-    const dd q = horner_comp_pos<N, KC>(Q, z.hi, z.lo);
+    const dd p = horner_comp_pos<N, KC, QM_DD_ZL_STEPS>(P, z.hi, z.lo);
+    const dd q = horner_comp_pos<N, KC, QM_DD_ZL_STEPS>(Q, z.hi, z.lo);
     double r = rcp_approx_f64(q.hi);
     r = __fma_rn(r, __fma_rn(-q.hi, r, 1.0), r);
     const double q0 = __dmul_rn(p.hi, r);

@@ -316,3 +316,23 @@ def test_d13_partial_compensation_bound():
     assert mx(8, 12.0) < 0.9
     assert mx(10, 36.04) < 0.6
     assert mx(9, 36.04) > 1.5          # the bound is what rules 9 steps out (measured 2.13 ulp on B200)
+
+    # z's low part enters the product once, as zl R(zh) (rational_dd): the dropped
+    # zh zl R'(zh) is (zl/zh)(kappa - 1) of the result, |zl/zh| <= 2^-53, with
+    # kappa - 1 = z (P'/P - Q'/Q) -- the logarithmic derivative of R, here from the
+    # coefficients, pinned below against the closed form of the exact map
+    # w(z) = Phi^-1(1 - e^-z/2): kappa = z w'/w, w' = (e^-z/2)/phi(w).
+    def km1(z):
+        i = np.arange(p.size)
+        dp = (p * i * z ** np.maximum(i - 1, 0)).sum() / (p * z ** i).sum()
+        dq = (q * i * z ** np.maximum(i - 1, 0)).sum() / (q * z ** i).sum()
+        return z * (dp - dq)
+
+    for z in (0.5, 3.0, 12.0, 30.0):
+        w = float(O.Q_exact(np.array([z]))[0])
+        phi = np.exp(-0.5 * w * w) / np.sqrt(2 * np.pi)
+        assert abs((1 + km1(z)) - z * (0.5 * np.exp(-z) / phi) / w) < 1e-12
+    zs = np.linspace(0.0, 36.04, 4001)
+    assert max(abs(km1(z)) for z in zs) < 0.48
+    total = max(W(p, z, 10) + W(q, z, 10) + abs(km1(z)) for z in zs)
+    assert total + 0.5 < 1.6           # <= 1.54 ulp: inside the 2-ulp contract
