@@ -400,6 +400,17 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
         "student_moments")
     ws = torch.empty(4 * Q.qm_moment_row_count(1 << 30), dtype=torch.float64, device="cuda")
     rec("moments_f64_2^30", lambda: Q.qm_moments(tt, 4, rows=ws), 1 << 30, 8, "hbm", "moments")
+    # a read-only stream is not bounded by the copy (read + write) peak: its roofline
+    # takes a read-only peak measured here, a library reduction over the same 8 GiB
+    acc = torch.empty((), dtype=torch.float64, device="cuda")
+    ms_rd = time_steps(lambda: torch.sum(tt, dim=0, out=acc), steps, warmup) / steps
+    rd = 8 * (1 << 30) / (ms_rd / 1e3) / 1e9
+    m = out["moments_f64_2^30"]
+    pk = max(rd, peaks["hbm_gbs"])
+    m["roofline"].update({"peak": pk, "frac": m["roofline"]["achieved"] / pk,
+                          "copy_peak_frac": m["roofline"]["achieved"] / peaks["hbm_gbs"],
+                          "peak_source": f"read-only stream: torch.sum over the same 8 GiB fp64 in this run "
+                                         f"({rd:.0f} GB/s), or the copy peak if higher"})
     del zn, tt, rows4, ws
     # config 5 building block: Laplace -> normal
     from synth import inputs as I

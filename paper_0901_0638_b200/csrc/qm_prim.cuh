@@ -63,8 +63,14 @@ QM_DEV float min3_nan(float a, float b, float c)
 
 // Packed fp32 pair arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): two
 // independent IEEE round-to-nearest operations per instruction.
+// QM_F32X2 (A/B): 1 = packed instructions; 0 = two scalar ones each (bitwise the
+// same results); 2 = packed FFMA2 only, scalar adds and multiplies
+#ifndef QM_F32X2
+#define QM_F32X2 1
+#endif
 QM_DEV float2 fma2(float2 a, float2 b, float2 c)
 {
+    if (QM_F32X2 == 0) return make_float2(__fmaf_rn(a.x, b.x, c.x), __fmaf_rn(a.y, b.y, c.y));
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
         "mov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tmov.b64 rc, {%6,%7};\n\t"
@@ -76,6 +82,7 @@ QM_DEV float2 fma2(float2 a, float2 b, float2 c)
 }
 QM_DEV float2 mul2(float2 a, float2 b)
 {
+    if (QM_F32X2 != 1) return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
         "mov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
@@ -86,6 +93,7 @@ QM_DEV float2 mul2(float2 a, float2 b)
 }
 QM_DEV float2 add2(float2 a, float2 b)
 {
+    if (QM_F32X2 != 1) return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
         "mov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"

@@ -1,0 +1,28 @@
+"""Max and tail-quantile ulp error of the fp64 breakless maps against the oracle
+(measurement helper, not a test): python tools/f64_ulp.py [log2 n]
+Inputs: half odd-grid uniforms, half tail-stratified (min(u, 1-u) log-uniform
+down to 2^-53), the parity tests' recipe at a larger size.  One JSON line per formula."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+import oracle as O  # noqa: E402
+import paper_0901_0638_b200 as Q  # noqa: E402
+from _parity import ulp_errors  # noqa: E402
+from synth import inputs as I  # noqa: E402
+
+n = 1 << int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 22
+u = np.concatenate([I.uniform_grid(n // 2, dtype=np.float64), I.tail_stratified(n - n // 2, dtype=np.float64)])
+ud = torch.from_numpy(u).cuda()
+for name, alg, form in (("D13", Q.BREAKLESS, O.D13), ("F1212", Q.BREAKLESS1212, O.F1212),
+                        ("A77", Q.BREAKLESS77, O.A77)):
+    z = Q.qm_normal_quantile(ud, alg=alg).cpu().numpy()
+    e = ulp_errors(z, O.normal_breakless(u, form, 64), np.float64)
+    print(json.dumps({"formula": name, "n": int(n), "max_ulp": float(e.max()),
+                      "p99999_ulp": float(np.quantile(e, 0.99999)), "mean_ulp": float(e.mean()),
+                      "lib": os.environ.get("QM_LIB_PATH", "libqm.so")}), flush=True)
