@@ -98,12 +98,35 @@ struct RodePrep {
 struct RodeBounds {
     double wc0, wc1, v0, v1, vm0, vm1;
     double iwc0, iwc1;   // 1/Wc per side (the centre record's 1/h slot when graded or on octaves)
+    double nu, nu1;      // Student table: n and n + 1 (table[2]); R'' from the RODE (rode_student_d2)
 };
 QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 {
+    const double nu = __ldg(tab + 2);
     return RodeBounds{__ldg(tab + QM_RODE_SEG + 8), __ldg(tab + QM_RODE_SEG + 24 + 8),
                       __ldg(tab + QM_RODE_SEG + 16), __ldg(tab + QM_RODE_SEG + 24 + 16),
-                      __ldg(tab + 28), __ldg(tab + 29), __ldg(tab + QM_RODE_SEG + 2), __ldg(tab + QM_RODE_SEG + 24 + 2)};
+                      __ldg(tab + 28), __ldg(tab + 29), __ldg(tab + QM_RODE_SEG + 2), __ldg(tab + QM_RODE_SEG + 24 + 2),
+                      nu, nu + 1.0};
+}
+
+// R'' of the Student table's centre nodes from the RODE itself instead of a third
+// shared load (the table stores the same quantity, rounded from long double):
+//     R'' = H(R) R'^2 - w R',  H(R) = (n + 1) R / (n + R^2)      (Gaussian base)
+// at the node w.  The map was bound by the shared-memory data pipe (89 % of its peak:
+// random 8-byte gathers cost ~6 wavefronts per warp for 256 bytes); dropping the R''
+// loads trades 2 of the 4 gathers per sample for ~14 FP64 operations.  The second
+// derivative enters the quintic with weight ~(h/w)^2 < 1e-5, so the ~2^-45 relative
+// error of this evaluation (one Newton step on the reciprocal) is below 1e-19 of R.
+#ifndef QM_RODE_ODE_D2
+#define QM_RODE_ODE_D2 1   // A/B: 0 = R'' from shared memory like the other tables
+#endif
+QM_DEV double rode_student_d2(double r, double rp, double w, const RodeBounds &bd)
+{
+    const double s = __fma_rn(r, r, bd.nu);
+    double q = rcp_approx_f64(s);
+    q = __fma_rn(q, __fma_rn(-s, q, 1.0), q);
+    const double H = __dmul_rn(__dmul_rn(bd.nu1, r), q);
+    return __dmul_rn(rp, __fma_rn(rp, H, -w));
 }
 
 // one double from shared memory by its 32-bit shared address (an explicit LDS,
@@ -304,6 +327,9 @@ QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd
 
 // B samples x[i] = Q(v[i]), in groups of up to 4 whose node gathers are all
 // issued before their arithmetic (4 keeps the state in registers)
+#ifndef QM_RODE_G
+#define QM_RODE_G 4   // A/B knob: samples per gather group
+#endif
 // SIDES = 1 (odd map): side 0 for |v|, the sign of v at the end
 QM_DEV double rode_odd(double v, double q) { return v < 0.0 ? -q : q; }
 
@@ -311,8 +337,8 @@ template <int M, int MODE, int SIDES = 2, int B>
 QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, const RodeBounds &bd, const double (&v)[B],
                            double (&x)[B])
 {
-    constexpr int G = B < 4 ? B : 4;
-    static_assert(B % G == 0, "batch must split into groups of 4");
+    constexpr int G = B < QM_RODE_G ? B : QM_RODE_G;
+    static_assert(B % G == 0, "batch must split into groups of QM_RODE_G");
 #pragma unroll
     for (int g = 0; g < B; g += G) {
         if constexpr ((MODE & kRodeOct) && M > 0) {
@@ -330,7 +356,13 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
 #pragma unroll
                 for (int k = 0; k < G; ++k) {
                     const double2 n0 = lds_f64x2(f[k].addr), n1 = lds_f64x2(f[k].addr + 16);
-                    nd[k] = RodeNodes{n0.x, n0.y, lds_f64(f[k].addr2), n1.x, n1.y, lds_f64(f[k].addr2 + 8)};
+                    if constexpr (SIDES == 1 && (MODE & kRodeLog) && QM_RODE_ODE_D2) {   // Student table
+                        const double w0 = __fma_rn(-f[k].p.t, f[k].p.ws0, f[k].p.a), w1 = w0 + f[k].p.ws0;
+                        nd[k] = RodeNodes{n0.x, n0.y, rode_student_d2(n0.x, n0.y, w0, bd),
+                                          n1.x, n1.y, rode_student_d2(n1.x, n1.y, w1, bd)};
+                    } else {
+                        nd[k] = RodeNodes{n0.x, n0.y, lds_f64(f[k].addr2), n1.x, n1.y, lds_f64(f[k].addr2 + 8)};
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < G; ++k) {

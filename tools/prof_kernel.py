@@ -83,14 +83,17 @@ def make(name):
         v = torch.from_numpy(I.laplace(n + 1, dtype=np.float64)).cuda()[1:]
         x = torch.empty(n + 1, dtype=torch.float64, device="cuda")[1:]
         fn = lambda: Q.qm_recycle_exp_to_hyperbolic(v, tab, out=x)
-    elif name in ("rode_hyp_f64", "rode_philox_f32"):
-        import numpy as np
-        from synth import inputs as I
-        tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
-        if name == "rode_hyp_f64":
-            v = torch.from_numpy(I.laplace(n, dtype=np.float64)).cuda()
+    elif name in ("rode_hyp_f64", "rode_philox_f32", "rode_vg_real_f64"):
+        if name == "rode_vg_real_f64":
+            tab = Q.qm_exp_target_table(Q.VG, [2.7, 1.0, 0.5])
+        else:
+            tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
+        if name != "rode_philox_f32":
+            # the table's own exponential base from Philox uniforms
+            v = Q.qm_exp_base_quantile(Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64), tab)
             x = torch.empty_like(v)
-            fn = lambda: Q.qm_recycle_exp_to_hyperbolic(v, tab, out=x)
+            call = Q.qm_recycle_exp_to_vg if name == "rode_vg_real_f64" else Q.qm_recycle_exp_to_hyperbolic
+            fn = lambda: call(v, tab, out=x)
         else:
             x = torch.empty(n, dtype=torch.float32, device="cuda")
             fn = lambda: Q.qm_exp_target_philox(n, tab, SEED, 0, dtype=torch.float32, out=x)
