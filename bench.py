@@ -424,17 +424,17 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     tab_r = Q.qm_exp_target_table(Q.VG, [2.7, 1.0, 0.5])
     # inputs: each table's own exponential base (rates alpha -+ beta, masses p-+;
     # P:322-329), drawn by the library's base quantile from Philox uniforms (untimed)
-    u64 = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
-    x64 = torch.empty_like(u64)
-    v64 = Q.qm_exp_base_quantile(u64, tab_h)
+    ub64 = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
+    x64 = torch.empty_like(ub64)
+    v64 = Q.qm_exp_base_quantile(ub64, tab_h)
     rec("exp_to_hyperbolic_f64_2^28", lambda: Q.qm_recycle_exp_to_hyperbolic(v64, tab_h, out=x64), n, 16, "hbm",
         "rode_hyp_f64")
-    Q.qm_exp_base_quantile(u64, tab_v, out=v64)
+    Q.qm_exp_base_quantile(ub64, tab_v, out=v64)
     rec("exp_to_vg_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_v, out=x64), n, 16, "hbm")
-    Q.qm_exp_base_quantile(u64, tab_r, out=v64)
+    Q.qm_exp_base_quantile(ub64, tab_r, out=v64)
     rec("exp_to_vg_lambda2.7_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_r, out=x64), n, 16, "hbm",
         "rode_vg_real_f64")
-    del u64, v64, x64
+    del ub64, v64, x64
     xf = torch.empty(n, dtype=torch.float32, device="cuda")
     rec("hyperbolic_philox_f32_2^28", lambda: Q.qm_exp_target_philox(n, tab_h, SEED, 0, dtype=torch.float32, out=xf),
         n, 4, "issue", "rode_philox_f32")

@@ -423,21 +423,25 @@ QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 // z P(z)/Q(z) for a double-double z >= 0, one final rounding (positive
 // coefficients: the breakless rationals).
 // z's low part zl (|zl| <= 2^-53 zh) enters once, as zl R(zh) in the final sum,
-// not in every compensated Horner step (QM_DD_ZL_STEPS=1 restores the per-step
-// form): (zh + zl) R(zh + zl) = zh R + zl R + zh zl R' + O(zl^2), and the dropped
+// not in every compensated Horner step, for z on the fp64 grid (QM_DD_ZL_STEPS=1
+// restores the per-step form everywhere): (zh + zl) R(zh + zl) = zh R + zl R + zh zl R' + O(zl^2), and the dropped
 // zh zl R' is (zl/zh)(kappa - 1) of the result, kappa = d ln(zR)/d ln z.  On the
 // fp64 grid (z <= 36.04) |kappa - 1| <= 0.473 for App D, so this adds <= 0.473 ulp:
 // with the plain steps' W_P + W_Q it stays <= 1.04 + 0.5 (final rounding) ulp
 // (tests/test_oracle_normal.py::test_d13_partial_compensation_bound), and it saves
 // one DFMA per compensated step (20 of App D's ~211 FP64 operations per sample).
+// Off the fp64 grid (z > 36.05: u < 2^-53, only from callers' own uniforms) W_P + W_Q
+// grows (1.55 at z = 74) and the per-step form is kept there, per lane (a warp vote
+// skips it when no lane needs it): results depend on the lane's own z only.
 #ifndef QM_DD_ZL_STEPS
 #define QM_DD_ZL_STEPS 0
 #endif
-template <int N, int KC>
-QM_DEV double rational_dd(dd z, const double *P, const double *Q)
+#define QM_DD_ZL_ZMAX 36.05
+template <int N, int KC, bool ZL>
+QM_DEV double rational_dd_zl(dd z, const double *P, const double *Q)
 {
-    const dd p = horner_comp_pos<N, KC, QM_DD_ZL_STEPS>(P, z.hi, z.lo);
-    const dd q = horner_comp_pos<N, KC, QM_DD_ZL_STEPS>(Q, z.hi, z.lo);
+    const dd p = horner_comp_pos<N, KC, ZL>(P, z.hi, z.lo);
+    const dd q = horner_comp_pos<N, KC, ZL>(Q, z.hi, z.lo);
     double r = rcp_approx_f64(q.hi);
     r = __fma_rn(r, __fma_rn(-q.hi, r, 1.0), r);
     const double q0 = __dmul_rn(p.hi, r);
@@ -445,6 +449,17 @@ QM_DEV double rational_dd(dd z, const double *P, const double *Q)
     e = __fma_rn(-q0, q.lo, __dadd_rn(e, p.lo));
     const double dq = __dmul_rn(e, r);
     return __fma_rn(z.hi, q0, __fma_rn(z.hi, dq, __dmul_rn(z.lo, q0)));
+}
+template <int N, int KC>
+QM_DEV double rational_dd(dd z, const double *P, const double *Q)
+{
+    if (QM_DD_ZL_STEPS) return rational_dd_zl<N, KC, true>(z, P, Q);
+    double r = rational_dd_zl<N, KC, false>(z, P, Q);
+    if (__any_sync(__activemask(), z.hi > QM_DD_ZL_ZMAX)) {
+        const double r2 = rational_dd_zl<N, KC, true>(z, P, Q);
+        r = (z.hi > QM_DD_ZL_ZMAX) ? r2 : r;
+    }
+    return r;
 }
 
 QM_DEV double apply_sign_f64(double mag, double u, double omu)
