@@ -430,13 +430,15 @@ QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 // with the plain steps' W_P + W_Q it stays <= 1.04 + 0.5 (final rounding) ulp
 // (tests/test_oracle_normal.py::test_d13_partial_compensation_bound), and it saves
 // one DFMA per compensated step (20 of App D's ~211 FP64 operations per sample).
-// Off the fp64 grid (z > 36.05: u < 2^-53, only from callers' own uniforms) W_P + W_Q
-// grows (1.55 at z = 74) and the per-step form is kept there, per lane (a warp vote
-// skips it when no lane needs it): results depend on the lane's own z only.
+// Off the fp64 grid (z > 36.8: u below the odd grid's 2^-54, only from callers' own
+// uniforms, or Laplace |v| > 36.8) App D's plain steps weigh more (W_P + W_Q = 1.55 at
+// z = 74, -> 6 as z grows: 3.7 ulp measured at z = 477 with 10 of 13 steps), so there
+// rat64 evaluates all 13 steps compensated with zl per step (<= 0.5 + O(u) ulp), per
+// lane, out of line and only when a lane of the warp needs it.
 #ifndef QM_DD_ZL_STEPS
 #define QM_DD_ZL_STEPS 0
 #endif
-#define QM_DD_ZL_ZMAX 36.05
+#define QM_DD_ZL_ZMAX 36.8
 template <int N, int KC, bool ZL>
 QM_DEV double rational_dd_zl(dd z, const double *P, const double *Q)
 {
@@ -453,13 +455,7 @@ QM_DEV double rational_dd_zl(dd z, const double *P, const double *Q)
 template <int N, int KC>
 QM_DEV double rational_dd(dd z, const double *P, const double *Q)
 {
-    if (QM_DD_ZL_STEPS) return rational_dd_zl<N, KC, true>(z, P, Q);
-    double r = rational_dd_zl<N, KC, false>(z, P, Q);
-    if (__any_sync(__activemask(), z.hi > QM_DD_ZL_ZMAX)) {
-        const double r2 = rational_dd_zl<N, KC, true>(z, P, Q);
-        r = (z.hi > QM_DD_ZL_ZMAX) ? r2 : r;
-    }
-    return r;
+    return rational_dd_zl<N, KC, QM_DD_ZL_STEPS != 0>(z, P, Q);
 }
 
 QM_DEV double apply_sign_f64(double mag, double u, double omu)
@@ -530,6 +526,13 @@ QM_DEV float rat32(float z)
     return rational_f32path<6>(z, kC55P, kC55Q);
 }
 
+// App D with all 13 Horner steps compensated and zl per step (off the grid; out of
+// line so that the hot loop keeps its registers)
+__device__ __noinline__ double d13_full(double zh, double zl)
+{
+    return rational_dd_zl<14, 13, true>(dd{zh, zl}, kD13P, kD13Q);
+}
+
 template <int ALG>
 QM_DEV double rat64(dd z)
 {
@@ -553,7 +556,12 @@ QM_DEV double rat64(dd z)
     if (QM_D13_SPLIT)
         return (z.hi <= QM_D13_ZSPLIT) ? rational_dd<14, QM_D13_KC_LO>(z, kD13P, kD13Q)
                                         : rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
-    return rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+    double r = rational_dd<14, QM_D13_KC>(z, kD13P, kD13Q);
+    if (__any_sync(__activemask(), z.hi > QM_DD_ZL_ZMAX)) {     // off the grid (above)
+        const double rf = d13_full(z.hi, z.lo);
+        r = (z.hi > QM_DD_ZL_ZMAX) ? rf : r;
+    }
+    return r;
 }
 
 // The same value in warp-uniform code: every lane evaluates the cheap scheme; if

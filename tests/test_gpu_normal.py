@@ -55,6 +55,26 @@ def test_fp32_breakless_exhaustive_grid():
     assert np.array_equal(g[n:], -g[:n])
 
 
+@pytest.mark.parametrize("n", [20000, (1 << 22) + 37])          # LDG kernels / TMA pipeline
+def test_fp64_off_grid_inputs(n):
+    """Uniforms far below the 2^-54 odd grid (u = 10^U(-320, -16): z = 36 .. 736) and
+    Laplace |v| up to 745 -- where App D's ten compensated steps are not enough (3.7 ulp
+    measured at z = 477) and rat64 switches those lanes to the fully compensated form
+    (qm_math.cuh): 2 ulp of the oracle, in warps mixed with on-grid samples."""
+    rng = np.random.default_rng(21)
+    u = 10.0 ** rng.uniform(-320, -16, n)
+    u = np.where(rng.uniform(size=n) < 0.5, u, I.uniform_grid(n, dtype=np.float64))   # mixed warps
+    u[1::7] = 1 - u[1::7]
+    for alg, form in ((Q.BREAKLESS, O.D13), (Q.BREAKLESS77, O.A77)):
+        err = ulp_errors(_gpu(Q.qm_normal_quantile, u, alg=alg), O.normal_breakless(u, form, 64), np.float64)
+        assert err.max() <= 2.0, summary(err)
+        err = ulp_errors(_gpu(Q.qm_normal_antithetic, u, alg=alg), O.normal_antithetic(u, form, 64), np.float64)
+        assert err.max() <= 2.0, summary(err)
+    v = rng.uniform(-745, 745, n)
+    err = ulp_errors(_gpu(Q.qm_recycle_exp_to_normal, v), O.exp_to_normal(v, O.D13, 64), np.float64)
+    assert err.max() <= 2.0, summary(err)
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("n", [0, 1, 3, 5, 63, 4097])
 @pytest.mark.parametrize("offset", [0, 1])
