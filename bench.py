@@ -463,7 +463,7 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
                 for _ in range(100):
                     call(u1, out=z1, alg=alg)
             key = {"breakless_D13": "config1_breakless", "as241": "config1_as241", "acklam": "config1_acklam",
-                   "acklam_refined": "config1_refined", "moro": "config1_moro", "breakless77": None}[name]
+                   "acklam_refined": "config1_refined", "moro": "config1_moro", "breakless77": "config1_breakless77"}[name]
             rec(f"config1_f64_2^20_{scheme}{name}", graph.replay, 100 << 20, 16, "fp64",
                 (("plain_" if scheme else "") + key) if key else None,
                 extra={"timing": "CUDA graph of 100 launches per step",

@@ -27,6 +27,9 @@ if [ "${PROFS:-all}" != all ] && [ "${PROFS}" != none ]; then
   want config1_breakless && prof config1_breakless "k_normal_f64" "" config1_breakless
   want fused_f32 && prof fused_f32 k_philox_f32
   want rode_hyp_f64 && prof rode_hyp_f64 k_rode_map_tl
+  want student_rode && prof student_rode k_rode_map_tl
+  want stream_f64_1212 && prof stream_f64_1212 k_normal_f64
+  want rode_vg_real_f64 && prof rode_vg_real_f64 k_rode_map_tl
 fi
 if [ "${PROFS:-all}" = all ]; then
   prof stream_f32 k_normal_f32_tl; cp /tmp/prof_stream_f32.ncu-rep $OUT/
@@ -45,7 +48,7 @@ if [ "${PROFS:-all}" = all ]; then
   prof rode_hyp_f64 k_rode_map_tl
   prof rode_philox_f32 k_rode_philox
   prof two_region k_normal_f32_tl "" stream_f32_two
-  for a in breakless as241 acklam refined moro; do
+  for a in breakless as241 acklam refined moro breakless77; do
     prof config1_$a "k_normal_f64|k_branchy" "" config1_$a
     prof plain_config1_$a k_plain_f64 "" plain_config1_$a
   done

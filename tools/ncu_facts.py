@@ -14,7 +14,7 @@ ELEMS = {"stream_f32": 1 << 28, "stream_f32_ldg": 1 << 28, "stream_f64": 1 << 28
          "student_moments": 1 << 30, "two_region": 1 << 28, "rode_hyp_f64": 1 << 28, "rode_philox_f32": 1 << 28,
          "stream_f64_1212": 1 << 28, "fused_f32_fma": 1 << 32, "student_k16": 1 << 30, "student_rode": 1 << 30,
          "rode_vg_real_f64": 1 << 28}
-for _a in ("breakless", "as241", "acklam", "refined", "moro"):      # config 1: one launch of 2^20
+for _a in ("breakless", "as241", "acklam", "refined", "moro", "breakless77"):      # config 1: one launch of 2^20
     ELEMS[f"config1_{_a}"] = 1 << 20
     ELEMS[f"plain_config1_{_a}"] = 1 << 20
 

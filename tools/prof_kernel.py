@@ -33,7 +33,7 @@ def make(name):
         import numpy as np
         from synth import inputs as I
         alg = {"breakless": Q.BREAKLESS, "as241": Q.AS241, "acklam": Q.ACKLAM, "refined": Q.ACKLAM_REFINED,
-               "moro": Q.MORO}[name.split("config1_")[1]]
+               "moro": Q.MORO, "breakless77": Q.BREAKLESS77}[name.split("config1_")[1]]
         u = torch.from_numpy(I.tail_stratified(1 << 20, dtype=np.float64)).cuda()
         z = torch.empty_like(u)
         call = Q.qm_normal_quantile_plain if name.startswith("plain_") else Q.qm_normal_quantile
