@@ -117,8 +117,12 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 // loads trades 2 of the 4 gathers per sample for ~14 FP64 operations.  The second
 // derivative enters the quintic with weight ~(h/w)^2 < 1e-5, so the ~2^-45 relative
 // error of this evaluation (one Newton step on the reciprocal) is below 1e-19 of R.
+// A/B only (measured +1.2 %, 219.6 -> 222.1 Gsamples/s): the generic path keeps the
+// stored R'', so a sample's last bit would depend on whether its warp took the fast
+// path -- the product keeps one R'' for every path (the same experiment on the
+// hyperbolic table, with a reciprocal square root per node, measured -2.5 %).
 #ifndef QM_RODE_ODE_D2
-#define QM_RODE_ODE_D2 1   // A/B: 0 = R'' from shared memory like the other tables
+#define QM_RODE_ODE_D2 0   // A/B: 1 = the Student centre's R'' from the RODE in the fast path
 #endif
 QM_DEV double rode_student_d2(double r, double rp, double w, const RodeBounds &bd)
 {

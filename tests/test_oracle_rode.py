@@ -322,3 +322,31 @@ def test_product_student_table_rejects():
     for nu in (0.5, 0.0, -1.0, 201.0, float("nan")):
         with pytest.raises(ValueError):
             qm_rode_table_host(STUDENT, [nu])
+
+@pytest.mark.parametrize("kind,par", [("hyp", [1.0, 0.5, 1.0]), ("hyp", [2.0, -0.7, 0.3]), ("student", [3.0]),
+                                      ("student", [1.0])])
+def test_centre_second_derivative_is_the_rode(kind, par):
+    """The stored R'' of the centre nodes (the builder's long double, rounded) is the
+    RODE evaluated at the stored (R, R') and the node -- R'' = H(R) R'^2 - w R'
+    (Gaussian base) or H(R) R'^2 - rate R' (exponential base), H = -(log f)' of the
+    target -- within rounding (also what the A/B fast path
+    QM_RODE_ODE_D2 = 1 of qm_rode.cuh computes on the fly)."""
+    from paper_0901_0638_b200.qm import HYPERBOLIC, STUDENT, qm_rode_table_host
+    tab = qm_rode_table_host(HYPERBOLIC if kind == "hyp" else STUDENT, par)
+    H, SEG, NT = 80, 32, int(tab[1])
+    ks = np.arange(0, 3584, 7)
+    for side in ((0, 1) if kind == "hyp" else (0,)):
+        nd = tab[H + side * 4 * (NT + 1):H + (side + 1) * 4 * (NT + 1)].reshape(-1, 4)[ks]
+        r, rp, rpp = nd[:, 0], nd[:, 1], nd[:, 2]
+        if kind == "hyp":
+            a, b, d = par
+            Hr = a * r / np.sqrt(d * d + r * r) - b
+            f = Hr * rp * rp - tab[10 + side] * rp
+        else:
+            n = par[0]
+            assert tab[2] == n
+            w = _node_w(tab, side, 0, ks)
+            f = (n + 1) * r / (n + r * r) * rp * rp - w * rp
+        scale = np.abs(Hr * rp * rp if kind == "hyp" else (n + 1) * r / (n + r * r) * rp * rp) + np.abs(
+            (tab[10 + side] if kind == "hyp" else w) * rp)
+        assert np.all(np.abs(f - rpp) <= 1e-14 * scale + 1e-300), np.max(np.abs(f - rpp) / scale)
