@@ -296,6 +296,8 @@ def variant_roofline(bound, gsamples, bytes_per, fact, peaks, sms):
     bench's rate) vs 148 SMs x 4 SMSPs x 0.5/cycle x the max SM clock; issue: all
     warp-instructions/s vs 1/cycle/SMSP."""
     clk = peaks["sm_max_mhz"] / 1e3                                # GHz
+    if bound == "smem" and not (fact and fact.get("smem_wavefronts_per_elem")):
+        bound = "hbm"                                               # no shared-pipe count captured
     if bound == "hbm":
         ach = bytes_per * gsamples
         return {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -303,6 +305,16 @@ def variant_roofline(bound, gsamples, bytes_per, fact, peaks, sms):
                 "peak_source": peaks["source"]}
     if not fact:
         return None
+    if bound == "smem" and fact.get("smem_wavefronts_per_elem"):
+        # random shared-memory gathers (the RODE maps): data-pipe wavefronts per sample
+        # (ncu) x the bench's rate vs 1 wavefront per cycle per SM
+        ach = fact["smem_wavefronts_per_elem"] * gsamples
+        pk = sms * clk
+        return {"bound": "smem", "achieved": ach, "peak": pk, "unit": "G shared wavefronts/s", "frac": ach / pk,
+                "smem_wavefronts_per_sample": fact["smem_wavefronts_per_elem"],
+                "hbm_frac": bytes_per * gsamples / peaks["hbm_gbs"],
+                "peak_source": "148 SMs x 1 shared-memory wavefront per cycle x max SM clock",
+                "source": fact.get("source")}
     if bound == "fp64" and fact.get("fp64_inst_per_elem"):
         ach = fact["fp64_inst_per_elem"] * gsamples
         pk = sms * 4 * FP64_WARP_INST_PER_CYCLE_SMSP * clk
@@ -392,7 +404,7 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     for nu in (3.0, 5.0, 10.0):
         tab_s = Q.qm_normal_target_table(Q.STUDENT, [nu])
         rec(f"student_rode_f64_nu{int(nu)}_2^30", lambda tab_s=tab_s: Q.qm_recycle_normal_to_t_rode(zn, tab_s, out=tt),
-            1 << 30, 16, "hbm", "student_rode" if nu == 5.0 else None)
+            1 << 30, 16, "smem", "student_rode")
     del tab_s
     rows4 = torch.empty((Q.qm_moment_row_count(1 << 30), 4), dtype=torch.float64, device="cuda")
     rec("student_moments_f64_nu5_K16_2^30",
@@ -427,10 +439,10 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     ub64 = Q.qm_philox_uniform(n, SEED, 0, dtype=torch.float64)
     x64 = torch.empty_like(ub64)
     v64 = Q.qm_exp_base_quantile(ub64, tab_h)
-    rec("exp_to_hyperbolic_f64_2^28", lambda: Q.qm_recycle_exp_to_hyperbolic(v64, tab_h, out=x64), n, 16, "hbm",
+    rec("exp_to_hyperbolic_f64_2^28", lambda: Q.qm_recycle_exp_to_hyperbolic(v64, tab_h, out=x64), n, 16, "smem",
         "rode_hyp_f64")
     Q.qm_exp_base_quantile(ub64, tab_v, out=v64)
-    rec("exp_to_vg_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_v, out=x64), n, 16, "hbm")
+    rec("exp_to_vg_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_v, out=x64), n, 16, "smem", "rode_hyp_f64")
     Q.qm_exp_base_quantile(ub64, tab_r, out=v64)
     rec("exp_to_vg_lambda2.7_f64_2^28", lambda: Q.qm_recycle_exp_to_vg(v64, tab_r, out=x64), n, 16, "hbm",
         "rode_vg_real_f64")

@@ -91,6 +91,7 @@ struct RodePrep {
     double ws0, ws1, wss0, wss1;
     bool lg;             // segment holds log |R| (Student coarse tail): the value is +-exp(q)
     bool neg;            // side 1 (v < 0)
+    bool oc;             // on the octave-level centre (j = 0): R'' from the RODE when QM_RODE_ODE_D2
 };
 
 // per-side segment boundaries Wc, V and Vmax, held in registers (loaded once
@@ -117,12 +118,12 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 // loads trades 2 of the 4 gathers per sample for ~14 FP64 operations.  The second
 // derivative enters the quintic with weight ~(h/w)^2 < 1e-5, so the ~2^-45 relative
 // error of this evaluation (one Newton step on the reciprocal) is below 1e-19 of R.
-// A/B only (measured +1.2 %, 219.6 -> 222.1 Gsamples/s): the generic path keeps the
-// stored R'', so a sample's last bit would depend on whether its warp took the fast
-// path -- the product keeps one R'' for every path (the same experiment on the
-// hyperbolic table, with a reciprocal square root per node, measured -2.5 %).
+// The generic path (rode_map_batch) does the same for centre samples, so a sample's
+// bits do not depend on its warp's path; the fine and coarse segments keep the stored
+// R''.  (The same experiment on the hyperbolic table, with a reciprocal square root
+// per node, measured -2.5 %.)
 #ifndef QM_RODE_ODE_D2
-#define QM_RODE_ODE_D2 0   // A/B: 1 = the Student centre's R'' from the RODE in the fast path
+#define QM_RODE_ODE_D2 1   // A/B: 0 = the stored R'' on every path
 #endif
 QM_DEV double rode_student_d2(double r, double rp, double w, const RodeBounds &bd)
 {
@@ -228,6 +229,7 @@ QM_DEV RodePrep rode_prep(const double *__restrict__ tab, double v, const double
     p.wss0 = g4 ? 12.0 * r67.x * fk * fk : 0.0;
     p.wss1 = g4 ? 12.0 * r67.x * k1 * k1 : 0.0;
     p.lg = (MODE & kRodeLog) && j == 2;
+    p.oc = (MODE & kRodeOct) && j == 0 && r67.y == 1.0;
     p.neg = side != 0;
     return p;
 }
@@ -318,6 +320,7 @@ QM_DEV RodeFast rode_fast_prep(double v, uint32_t sm_nodes, const RodeBounds &bd
     f.p.ws0 = f.p.ws1 = c.h;
     f.p.wss0 = f.p.wss1 = 0.0;
     f.p.lg = false;
+    f.p.oc = true;
     f.p.neg = side != 0;
     f.p.b = f.p.b2 = nullptr;
     f.p.st = 2;
@@ -381,7 +384,15 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
 #pragma unroll
         for (int k = 0; k < G; ++k) p[k] = rode_prep<M, MODE, SIDES>(tab, v[g + k], sm, bd);
 #pragma unroll
-        for (int k = 0; k < G; ++k) nd[k] = rode_load<M>(p[k]);
+        for (int k = 0; k < G; ++k) {
+            nd[k] = rode_load<M>(p[k]);
+            if constexpr (SIDES == 1 && (MODE & kRodeLog) && (MODE & kRodeOct) && QM_RODE_ODE_D2) {
+                // the fast path's R'' for centre samples in the generic path too, bit for bit
+                const double w0 = __fma_rn(-p[k].t, p[k].ws0, p[k].a), w1 = w0 + p[k].ws0;
+                nd[k].dd0 = p[k].oc ? rode_student_d2(nd[k].r0, nd[k].d0, w0, bd) : nd[k].dd0;
+                nd[k].dd1 = p[k].oc ? rode_student_d2(nd[k].r1, nd[k].d1, w1, bd) : nd[k].dd1;
+            }
+        }
 #pragma unroll
         for (int k = 0; k < G; ++k) {
             const double q = rode_unlog<MODE>(p[k], rode_finish<MODE>(p[k], nd[k]));

@@ -33,8 +33,10 @@ for name, n in ELEMS.items():
                  "fp64_inst_per_elem": (k.get("fp64_pipe_pct", 0) / 100 * 592 * 0.5 *
                                         k.get("duration_us", 0) * 1e-6 * k.get("sm_clock_hz", 0) / n),
                  "source": f"{p} (ncu --set full, one launch of {n} samples)"}
+    if k.get("smem_wavefronts"):       # shared-memory data-pipe wavefronts (the RODE maps' gathers)
+        out[name]["smem_wavefronts_per_elem"] = k["smem_wavefronts"] / n
     for key in ("fp64_pipe_pct", "fma_pipe_pct", "alu_pipe_pct", "xu_pipe_pct", "issue_active_pct",
-                "divergent_branch_targets", "threads_per_inst", "registers"):
+                "divergent_branch_targets", "threads_per_inst", "registers", "smem_pipe_pct"):
         if key in k:
             out[name][key] = k[key]
 json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)

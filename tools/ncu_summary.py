@@ -28,6 +28,9 @@ KEYS = {
     "fp64_inst_executed": "smsp__inst_executed_pipe_fp64.sum",
     "fma_cycles_active": "sm__pipe_fma_cycles_active.sum",
     "sm_clock_hz": "sm__cycles_elapsed.avg.per_second",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "smem_pipe_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "smem_bank_conflicts": "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
 }
