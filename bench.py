@@ -404,7 +404,7 @@ def variants(Q, torch, peaks, steps=10, warmup=3):
     for nu in (3.0, 5.0, 10.0):
         tab_s = Q.qm_normal_target_table(Q.STUDENT, [nu])
         rec(f"student_rode_f64_nu{int(nu)}_2^30", lambda tab_s=tab_s: Q.qm_recycle_normal_to_t_rode(zn, tab_s, out=tt),
-            1 << 30, 16, "smem", "student_rode")
+            1 << 30, 16, "fp64", "student_rode")
     del tab_s
     rows4 = torch.empty((Q.qm_moment_row_count(1 << 30), 4), dtype=torch.float64, device="cuda")
     rec("student_moments_f64_nu5_K16_2^30",

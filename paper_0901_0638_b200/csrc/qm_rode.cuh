@@ -100,6 +100,8 @@ struct RodeBounds {
     double wc0, wc1, v0, v1, vm0, vm1;
     double iwc0, iwc1;   // 1/Wc per side (the centre record's 1/h slot when graded or on octaves)
     double nu, nu1;      // Student table: n and n + 1 (table[2]); R'' from the RODE (rode_student_d2)
+    double ha, hb, hd2;  // hyperbolic table: alpha, beta, delta^2 (table[3..5]; rode_hyp_d2)
+    double rate0, rate1; // base rates per side (table[10 + s])
 };
 QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 {
@@ -107,7 +109,7 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
     return RodeBounds{__ldg(tab + QM_RODE_SEG + 8), __ldg(tab + QM_RODE_SEG + 24 + 8),
                       __ldg(tab + QM_RODE_SEG + 16), __ldg(tab + QM_RODE_SEG + 24 + 16),
                       __ldg(tab + 28), __ldg(tab + 29), __ldg(tab + QM_RODE_SEG + 2), __ldg(tab + QM_RODE_SEG + 24 + 2),
-                      nu, nu + 1.0};
+                      nu, nu + 1.0, __ldg(tab + 3), __ldg(tab + 4), __ldg(tab + 5), __ldg(tab + 10), __ldg(tab + 11)};
 }
 
 // R'' of the Student table's centre nodes from the RODE itself instead of a third
@@ -123,8 +125,20 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 // R''.  (The same experiment on the hyperbolic table, with a reciprocal square root
 // per node, measured -2.5 %.)
 #ifndef QM_RODE_ODE_D2
-#define QM_RODE_ODE_D2 1   // A/B: 0 = the stored R'' on every path
+#define QM_RODE_ODE_D2 1   // A/B: 0 = the stored R'' on every path; 2 = also the hyperbolic table's
 #endif
+// the same for the hyperbolic table (exponential base):
+//     R'' = H(R) R'^2 - rate_s R',  H(x) = alpha x / sqrt(delta^2 + x^2) - beta
+// (1/sqrt from MUFU.RSQ64H and one Newton step: ~2^-46; the weight of R'' is < 1e-5)
+QM_DEV double rode_hyp_d2(double r, double rp, double rate, const RodeBounds &bd)
+{
+    const double s = __fma_rn(r, r, bd.hd2);
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+    y = __fma_rn(__dmul_rn(0.5, y), __fma_rn(-s, __dmul_rn(y, y), 1.0), y);
+    const double H = __fma_rn(__dmul_rn(bd.ha, r), y, -bd.hb);
+    return __dmul_rn(rp, __fma_rn(H, rp, -rate));
+}
 QM_DEV double rode_student_d2(double r, double rp, double w, const RodeBounds &bd)
 {
     const double s = __fma_rn(r, r, bd.nu);
@@ -155,11 +169,14 @@ QM_DEV double sel_f64(bool c, double a, double b)
 // so that each table pays only for its own: bit 0 = centre nodes at Wc (k/n)^4
 // (table[32 + 7] = 4), bit 2 = centre on octave levels (= 1), bit 1 = log-valued
 // segment 2 (Student, table[31])
-constexpr int kRodeGraded = 1, kRodeLog = 2, kRodeOct = 4;
+// bit 3 = hyperbolic octave table (R'' from the RODE, QM_RODE_ODE_D2 >= 2)
+constexpr int kRodeGraded = 1, kRodeLog = 2, kRodeOct = 4, kRodeHyp = 8;
 QM_DEV int rode_mode(const double *__restrict__ tab)
 {
     const double g = __ldg(tab + QM_RODE_SEG + 7);
-    return (g == 4.0 ? kRodeGraded : 0) | (g == 1.0 ? kRodeOct : 0) | (__ldg(tab + 31) != 0.0 ? kRodeLog : 0);
+    const bool hyp = QM_RODE_ODE_D2 >= 2 && g == 1.0 && __ldg(tab) == (double)QM_RODE_HYPERBOLIC;
+    return (g == 4.0 ? kRodeGraded : 0) | (g == 1.0 ? kRodeOct : 0) | (__ldg(tab + 31) != 0.0 ? kRodeLog : 0) |
+           (hyp ? kRodeHyp : 0);
 }
 
 // octave-level coordinate of x = w/Wc in [0, 1) (R36; L + 1 levels of NB intervals):
@@ -367,6 +384,10 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
                         const double w0 = __fma_rn(-f[k].p.t, f[k].p.ws0, f[k].p.a), w1 = w0 + f[k].p.ws0;
                         nd[k] = RodeNodes{n0.x, n0.y, rode_student_d2(n0.x, n0.y, w0, bd),
                                           n1.x, n1.y, rode_student_d2(n1.x, n1.y, w1, bd)};
+                    } else if constexpr (SIDES == 2 && (MODE & kRodeHyp)) {           // hyperbolic table
+                        const double rate = f[k].p.neg ? bd.rate1 : bd.rate0;
+                        nd[k] = RodeNodes{n0.x, n0.y, rode_hyp_d2(n0.x, n0.y, rate, bd),
+                                          n1.x, n1.y, rode_hyp_d2(n1.x, n1.y, rate, bd)};
                     } else {
                         nd[k] = RodeNodes{n0.x, n0.y, lds_f64(f[k].addr2), n1.x, n1.y, lds_f64(f[k].addr2 + 8)};
                     }
@@ -392,6 +413,11 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
                 nd[k].dd0 = p[k].oc ? rode_student_d2(nd[k].r0, nd[k].d0, w0, bd) : nd[k].dd0;
                 nd[k].dd1 = p[k].oc ? rode_student_d2(nd[k].r1, nd[k].d1, w1, bd) : nd[k].dd1;
             }
+            if constexpr (SIDES == 2 && (MODE & kRodeHyp)) {
+                const double rate = p[k].neg ? bd.rate1 : bd.rate0;
+                nd[k].dd0 = p[k].oc ? rode_hyp_d2(nd[k].r0, nd[k].d0, rate, bd) : nd[k].dd0;
+                nd[k].dd1 = p[k].oc ? rode_hyp_d2(nd[k].r1, nd[k].d1, rate, bd) : nd[k].dd1;
+            }
         }
 #pragma unroll
         for (int k = 0; k < G; ++k) {
@@ -406,6 +432,7 @@ QM_DEV void rode_map_batch(const double *__restrict__ tab, const double *sm, con
     switch (rode_mode(tab)) {                                                       \
     case kRodeOct: CALL(kRodeOct); break;                                           \
     case kRodeOct | kRodeLog: CALL(kRodeOct | kRodeLog); break;                     \
+    case kRodeOct | kRodeHyp: CALL(kRodeOct | kRodeHyp); break;                     \
     case kRodeGraded: CALL(kRodeGraded); break;                                     \
     default: CALL(kRodeGraded | kRodeOct | kRodeLog); break;                        \
     }

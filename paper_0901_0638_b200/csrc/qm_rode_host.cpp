@@ -456,6 +456,11 @@ bool rode_table_build(int kind, const double *params, double *tab)
     }
     tab[0] = kind;
     tab[1] = NT;
+    if (t.kind == QM_RODE_HYPERBOLIC) {   // the kernel's R'' = H(R) R'^2 - rate R' (rode_hyp_d2)
+        tab[3] = (double)t.a;
+        tab[4] = (double)t.b;
+        tab[5] = (double)(t.d * t.d);
+    }
     tab[30] = 3;
     return true;
 }

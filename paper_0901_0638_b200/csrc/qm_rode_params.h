@@ -14,6 +14,7 @@
 //                                        smallest double: every finite Q0(u) is interpolated)
 //
 // table[0]  kind (1 hyperbolic, 2 VG, 3 Student)   table[1]  NT (nodes per side - 1)   table[2] nu (Student)
+// table[3..5] alpha, beta, delta^2 (hyperbolic: the kernel's R'' from the RODE)
 // table[8+s] p_s (base mass: s=0 right p+, s=1 left p-)    table[10+s] rate_s (a-b right, a+b left)
 // table[12+s] Q(0) residual of the backward sweep           table[14+s] its slope residual
 // table[16+s], table[18+s]: log p_s as hi + lo              table[20+s] 1/rate_s

@@ -340,6 +340,7 @@ def test_centre_second_derivative_is_the_rode(kind, par):
         r, rp, rpp = nd[:, 0], nd[:, 1], nd[:, 2]
         if kind == "hyp":
             a, b, d = par
+            assert (tab[3], tab[4], tab[5]) == (a, b, d * d)          # the kernel's parameters
             Hr = a * r / np.sqrt(d * d + r * r) - b
             f = Hr * rp * rp - tab[10 + side] * rp
         else:
