@@ -122,8 +122,8 @@ QM_DEV RodeBounds rode_bounds(const double *__restrict__ tab)
 // error of this evaluation (one Newton step on the reciprocal) is below 1e-19 of R.
 // The generic path (rode_map_batch) does the same for centre samples, so a sample's
 // bits do not depend on its warp's path; the fine and coarse segments keep the stored
-// R''.  (The same experiment on the hyperbolic table, with a reciprocal square root
-// per node, measured -2.5 %.)
+// R''.  (The same for the hyperbolic table, QM_RODE_ODE_D2=2 with a reciprocal square
+// root per node, measured -11 % and stays off.)
 #ifndef QM_RODE_ODE_D2
 #define QM_RODE_ODE_D2 1   // A/B: 0 = the stored R'' on every path; 2 = also the hyperbolic table's
 #endif
