@@ -423,13 +423,13 @@ QM_DEV dd horner_comp_pos(const double *a, double zh, double zl)
 // z P(z)/Q(z) for a double-double z >= 0, one final rounding (positive
 // coefficients: the breakless rationals).
 // z's low part zl (|zl| <= 2^-53 zh) enters once, as zl R(zh) in the final sum,
-// not in every compensated Horner step, for z on the fp64 grid (QM_DD_ZL_STEPS=1
-// restores the per-step form everywhere): (zh + zl) R(zh + zl) = zh R + zl R + zh zl R' + O(zl^2), and the dropped
-// zh zl R' is (zl/zh)(kappa - 1) of the result, kappa = d ln(zR)/d ln z.  On the
-// fp64 grid (z <= 36.04) |kappa - 1| <= 0.473 for App D, so this adds <= 0.473 ulp:
-// with the plain steps' W_P + W_Q it stays <= 1.04 + 0.5 (final rounding) ulp
-// (tests/test_oracle_normal.py::test_d13_partial_compensation_bound), and it saves
-// one DFMA per compensated step (20 of App D's ~211 FP64 operations per sample).
+// not in every compensated Horner step (QM_DD_ZL_STEPS=1 restores the per-step
+// form): (zh + zl) R(zh + zl) = zh R + zl R + zh zl R' + O(zl^2), and the dropped
+// zh zl R' is (zl/zh)(kappa - 1) of the result, kappa = d ln(zR)/d ln z.  Up to
+// z = 36.8 (the fp64 grid ends at 36.04) |kappa - 1| < 0.48 for App D, so this adds
+// < 0.48 ulp: with the plain steps' W_P + W_Q it stays <= 1.06 + 0.5 (final rounding)
+// ulp (tests/test_oracle_normal.py::test_d13_partial_compensation_bound), and it
+// saves one DFMA per compensated step (20 of App D's ~211 FP64 operations per sample).
 // Off the fp64 grid (z > 36.8: u below the odd grid's 2^-54, only from callers' own
 // uniforms, or Laplace |v| > 36.8) App D's plain steps weigh more (W_P + W_Q = 1.55 at
 // z = 74, -> 6 as z grows: 3.7 ulp measured at z = 477 with 10 of 13 steps), so there

@@ -16,6 +16,10 @@ Q.qm_normal_quantile(u, alg=Q.TWO_REGION)
 Q.qm_recycle_exp_to_normal(torch.from_numpy(I.laplace(n, dtype=np.float32)).cuda())
 u64 = torch.from_numpy(I.mixed_uniforms(n, dtype=np.float64)).cuda()
 Q.qm_normal_quantile(u64)
+u64[::97] = 1e-300                                                      # off the grid: d13_full (out of line)
+Q.qm_normal_quantile(u64)
+Q.qm_normal_quantile(u64[1:])
+Q.qm_recycle_exp_to_normal(torch.linspace(-745, 745, n, dtype=torch.float64, device="cuda"))
 zn = torch.from_numpy(I.normals(n, dtype=np.float64)).cuda()
 Q.qm_recycle_normal_to_t(zn, 5.0, 16, 4.6506)
 tab = Q.qm_exp_target_table(Q.HYPERBOLIC, [1.0, 0.5, 1.0])
