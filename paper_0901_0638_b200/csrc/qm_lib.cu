@@ -229,6 +229,41 @@ qm_status student_setup(double nu, int K, double zstar, StudentParams *sp)
 
 }  // namespace
 
+// fp64 breakless map: the TMA-in / streaming-store pipeline for large aligned n,
+// else (and for the remainder) the LDG kernel -- every fp64 breakless formula
+template <int ALG>
+qm_status normal_f64(const double *ud, double *zd, int64_t n, int vec, cudaStream_t s)
+{
+    // the pipeline only pays with several tiles per CTA (small n: the LDG kernel
+    // balances better, e.g. config 1's 2^20: 55 vs 40 Gsamples/s)
+    if (vec && stream_path() == 2 && n >= ((int64_t)1 << 23)) {
+        static const int cfg = env_int("QM_TL64_CFG", 2, 0, 2);   // 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B (default: +2.3 % measured)
+        if (cfg > 0) {
+            auto go = [&](auto k, int tile, int threads, size_t smem) {
+                const int64_t ntiles = n / tile;
+                if (ntiles > 0) {
+                    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                        return QM_ECUDA;
+                    const int sms = sm_count_for_current_device();
+                    const int64_t gg = ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148);
+                    k<<<(int)gg, threads, smem, s>>>(ud, zd, ntiles);
+                }
+                const int64_t done = ntiles * tile;
+                if (n > done)
+                    k_normal_f64<ALG><<<grid_for(n - done, kThreads * 2, 8), kThreads, 0, s>>>(ud + done, zd + done,
+                                                                                      n - done, 1);
+                return launched();
+            };
+            if (cfg == 2) return go(k_normal_f64_tl<ALG, TlF64B>, TlF64B::TILE, TlF64B::THREADS,
+                                    (size_t)TlF64B::STAGES * TlF64B::TILE_VECS * 16);
+            return go(k_normal_f64_tl<ALG, TlF64A>, TlF64A::TILE, TlF64A::THREADS,
+                      (size_t)TlF64A::STAGES * TlF64A::TILE_VECS * 16);
+        }
+    }
+    k_normal_f64<ALG><<<grid_for(n, kThreads * 2, 8), kThreads, 0, s>>>(ud, zd, n, vec);
+    return launched();
+}
+
 extern "C" {
 
 int qm_abi_version(void) { return QM_ABI_VERSION; }
@@ -276,46 +311,12 @@ qm_status qm_normal_quantile(const void *u, void *z, int64_t n, qm_precision p, 
         k_branchy_f64<ALG_ACKLAM_REF><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n);
         return launched();
     case QM_MORO: k_branchy_f64<ALG_MORO><<<grid_for(n, kThreads, 8), kThreads, 0, s>>>(ud, zd, n); return launched();
-    case QM_BREAKLESS1212:
-        k_normal_f64<ALG_F1212><<<grid_for(n, kThreads * 2, 8), kThreads, 0, s>>>(ud, zd, n, vec);
-        return launched();
-    case QM_BREAKLESS88:
-        k_normal_f64<ALG_F88><<<grid_for(n, kThreads * 2, 8), kThreads, 0, s>>>(ud, zd, n, vec);
-        return launched();
+    case QM_BREAKLESS1212: return normal_f64<ALG_F1212>(ud, zd, n, vec, s);
+    case QM_BREAKLESS88: return normal_f64<ALG_F88>(ud, zd, n, vec, s);
     case QM_TWO_REGION: return QM_EUNSUPPORTED;
     default: break;
     }
-    const int g = grid_for(n, kThreads * 2, 8);
-    // the pipeline only pays with several tiles per CTA (small n: the LDG kernel
-    // balances better, e.g. config 1's 2^20: 55 vs 40 Gsamples/s)
-    if (alg == QM_BREAKLESS && vec && stream_path() == 2 && n >= ((int64_t)1 << 23)) {
-        static const int cfg = env_int("QM_TL64_CFG", 2, 0, 2);   // 0 = LDG kernel, 1 = TlF64A, 2 = TlF64B (default: +2.3 % measured)
-        if (cfg > 0) {
-            auto go = [&](auto k, int tile, int threads, size_t smem) {
-                const int64_t ntiles = n / tile;
-                if (ntiles > 0) {
-                    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-                        return QM_ECUDA;
-                    const int sms = sm_count_for_current_device();
-                    const int64_t gg = ntiles < (sms > 0 ? sms : 148) ? ntiles : (sms > 0 ? sms : 148);
-                    k<<<(int)gg, threads, smem, s>>>(ud, zd, ntiles);
-                }
-                const int64_t done = ntiles * tile;
-                if (n > done)
-                    k_normal_f64<ALG_BREAKLESS><<<grid_for(n - done, kThreads * 2, 8), kThreads, 0, s>>>(ud + done, zd + done,
-                                                                                                n - done, 1);
-                return launched();
-            };
-            if (cfg == 2) return go(k_normal_f64_tl<ALG_BREAKLESS, TlF64B>, TlF64B::TILE, TlF64B::THREADS,
-                                    (size_t)TlF64B::STAGES * TlF64B::TILE_VECS * 16);
-            return go(k_normal_f64_tl<ALG_BREAKLESS, TlF64A>, TlF64A::TILE, TlF64A::THREADS,
-                      (size_t)TlF64A::STAGES * TlF64A::TILE_VECS * 16);
-        }
-    }
-    return with_breakless(alg, [&](auto A) {
-        k_normal_f64<decltype(A)::value><<<g, kThreads, 0, s>>>(ud, zd, n, vec);
-        return launched();
-    });
+    return with_breakless(alg, [&](auto A) { return normal_f64<decltype(A)::value>(ud, zd, n, vec, s); });
 }
 
 qm_status qm_normal_quantile_plain(const void *u, void *z, int64_t n, qm_algorithm alg, void *stream)
